@@ -1,0 +1,179 @@
+/*
+ * taco_b200.h -- C ABI of the B200-native TACO compression path (sm_100a).
+ *
+ * The reference (arxiv/paper_2604_24088, /root/reference/proj) exposes the codec as a
+ * C++ header API over host spans; this ABI is what sits underneath the drop-in
+ * C++ layer (include/taco/{codec,fp8,...}.hpp, csrc/taco_cxx.cpp) and what
+ * non-C++ callers (ctypes, the NCCL collective driver) bind directly.  Each entry
+ * point names the reference interface it replaces.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only; no torch / CUDA types in signatures
+ *    (streams are passed as `void*` = cudaStream_t, NULL = legacy default stream).
+ *  - The device entry points never allocate and never synchronise: every buffer is
+ *    caller-owned device memory, work is enqueued on `stream`.
+ *  - Every function returns a taco_status; on error taco_last_error() holds the
+ *    reference's exact message (proj/include/taco/error.hpp:10-40 codes + 1).
+ *  - Data-dependent errors found by kernels (NaN/Inf input, bad block scalars) are
+ *    OR-ed into a caller-owned device int `d_flags` (may be NULL) and turned into
+ *    the reference's errors by taco_flags_status() once the stream is synchronised.
+ *
+ * Wire message layout (one per shard, or per shard-chunk), replacing the
+ * reference's AoS CompressedTensor (codec.hpp:37-49) / TACOCMP1 blocks
+ * (serialize.hpp:12-14) with an SoA that vector loads/stores can stream:
+ *      [ codes: nblocks*B bytes ][ pad to 16 ][ (alpha, scale) f32 pairs: nblocks*8 bytes ]
+ * msg_bytes = scal_offset + 8*nblocks (== nblocks*(B+8) whenever B >= 16, i.e. the
+ * reference's per-block wire cost, collective.cpp:50-58 minus the 22-byte archive
+ * header); msg_stride = msg_bytes rounded up to 16.
+ */
+#ifndef TACO_B200_H
+#define TACO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TACO_B200_ABI_VERSION 1
+
+typedef enum {
+    TACO_OK = 0,
+    TACO_ERR_USAGE = 1,   /* taco::ErrorCode::Usage   */
+    TACO_ERR_CONFIG = 2,  /* taco::ErrorCode::Config  */
+    TACO_ERR_INPUT = 3,   /* taco::ErrorCode::Input   */
+    TACO_ERR_IO = 4,      /* taco::ErrorCode::Io      */
+    TACO_ERR_CORRUPT = 5, /* taco::ErrorCode::Corrupt */
+    TACO_ERR_CUDA = 6     /* launch / runtime failure (no reference counterpart) */
+} taco_status;
+
+typedef enum { TACO_DT_F32 = 0, TACO_DT_BF16 = 1 } taco_dtype;
+
+/* d_flags bits */
+#define TACO_FLAG_NONFINITE_INPUT 1 /* -> Input,   "input tensor contains NaN or Inf"         */
+#define TACO_FLAG_BAD_SCALARS 2     /* -> Corrupt, "block scalars must be finite and nonzero" */
+
+/* taco::CodecConfig (codec.hpp:24-33).  kind: 0 = Taco (the only device kind);
+ * format: 0 = E4M3, 1 = E5M2 (fp8.hpp:8). */
+typedef struct {
+    uint32_t block_size;
+    float target_energy;
+    float stability_epsilon;
+    uint32_t format;
+    uint32_t kind;
+} taco_config;
+
+typedef struct {
+    uint64_t nblocks;
+    uint64_t codes_bytes; /* nblocks * B */
+    uint64_t scal_offset; /* codes_bytes rounded up to 16 */
+    uint64_t msg_bytes;   /* scal_offset + 8 * nblocks */
+    uint64_t msg_stride;  /* msg_bytes rounded up to 16 */
+} taco_layout;
+
+int taco_abi_version(void);
+const char* taco_last_error(void);
+/* thread-safe defaults: B=256, tau=1, eps=1e-12, E4M3, Taco (codec.hpp:24-33) */
+taco_config taco_default_config(void);
+
+/* taco::validate_config (codec.hpp:35; codec.cpp:189-197, transform.cpp:13-20) */
+int taco_validate_config(const taco_config* cfg);
+
+/* message geometry for `nblocks` blocks */
+int taco_msg_layout(const taco_config* cfg, uint64_t nblocks, taco_layout* out);
+
+/* ratio of the reference's wire layout, taco::compressed_ratio (codec.hpp:66) */
+double taco_compressed_ratio(const taco_config* cfg, uint64_t n);
+
+/* taco::archive_size_bytes (serialize.hpp:24): 22 + ceil(n/B)*(B+8) */
+uint64_t taco_archive_size(const taco_config* cfg, uint64_t n);
+
+/* Map the device flags word to the reference's error (TACO_OK if 0). */
+int taco_flags_status(int flags);
+
+/* ---------------------------------------------------------------- device API -------
+ * Shard geometry shared by the three kernels.  A logical input of n elements is cut
+ * into `shards` contiguous shards of S = ceil(n/shards) elements, zero-padded past n
+ * (collective.cpp:76-87); shard p is cut into ceil(S/B) blocks, zero-padded past S
+ * (codec.cpp:20-28).  [blk_begin, blk_end) selects a chunk of blocks of every shard
+ * (block-aligned chunking never changes numerics, test_collective.cpp:225-238).
+ * shards == 1 is the plain taco::compress / taco::decompress of one tensor.
+ */
+
+/* K1 -- fused ASH transform + dual-scale FP8 encode.  Replaces taco::compress
+ * (codec.hpp:57; codec.cpp:208-254 + rotate_block :45-62 + compress_block_taco
+ * :64-76).  Message for shard p goes to msgs + p*msg_stride. */
+int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
+                      uint32_t shards, uint64_t blk_begin, uint64_t blk_end, void* msgs,
+                      uint64_t msg_stride, int* d_flags, void* stream);
+
+/* K2 -- fused dequantise + inverse Hadamard + 1/alpha.  Replaces taco::decompress
+ * (codec.hpp:61-62; codec.cpp:264-296 + decompress_block :144-155).  Writes only
+ * the valid prefix of every shard (codec.cpp:151-153, collective.cpp:109). */
+int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_stride,
+                        uint32_t shards, uint64_t n, uint64_t blk_begin, uint64_t blk_end,
+                        void* out, int out_dtype, int* d_flags, void* stream);
+
+/* K3 -- fused decode of `nranks` messages of one shard, fp32 sum in ascending rank
+ * order, re-encode.  Replaces the owner loop of run_twoshot (collective.cpp:95-101):
+ * acc = dec(msg 0); acc += dec(msg r) for r = 1..P-1; compress(acc).
+ * Message r is read from msgs + r*rank_stride.  `shard_len` = S (positions >= S in
+ * the last block are re-zeroed before re-encoding).  acc_out (optional, may be NULL)
+ * receives the fp32 stage-1 sum for positions < S of the chunk (the SP reduce-scatter
+ * output and the stage-isolated parity hook), in acc_dtype. */
+int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride,
+                           uint32_t nranks, uint64_t shard_len, uint64_t blk_begin,
+                           uint64_t blk_end, void* out_msg, void* acc_out, int acc_dtype,
+                           int* d_flags, void* stream);
+
+/* In-process P-rank two-shot all-reduce on ONE device: the reference's RankSet
+ * simulation (taco::allreduce, collective.hpp:28, Algorithm::TwoShot,
+ * collective.cpp:75-111) with every "rank" a slice of `inputs` ([P][n], dtype).
+ * `work` must hold taco_allreduce_sim_workspace() bytes.  out: n elements in
+ * out_dtype (identical on every rank, so written once).  stage1 (optional): P*S fp32. */
+uint64_t taco_allreduce_sim_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n);
+int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype,
+                           uint32_t nranks, uint64_t n, void* out, int out_dtype, float* stage1,
+                           void* work, int* d_flags, void* stream);
+
+/* ------------------------------------------------------------------ host API -------
+ * Synchronous calls on host buffers, the shape of the reference's API (host spans in,
+ * host vectors out).  A context owns a stream, device buffers and pinned staging; the
+ * transfer is pipelined in chunks so H2D, kernels and D2H overlap. */
+typedef struct taco_ctx taco_ctx;
+
+int taco_ctx_create(int device, taco_ctx** out);
+void taco_ctx_destroy(taco_ctx* ctx);
+
+/* taco::compress on a host tensor: writes one message (layout for ceil(n/B) blocks)
+ * into msg_host (>= taco_msg_layout(...).msg_bytes).  Raises the reference's errors. */
+int taco_compress_host(taco_ctx* ctx, const taco_config* cfg, const void* x_host, int dtype,
+                       uint64_t n, void* msg_host);
+
+/* taco::decompress of one message into a host tensor of n elements */
+int taco_decompress_host(taco_ctx* ctx, const taco_config* cfg, const void* msg_host,
+                         uint64_t n, void* out_host, int out_dtype);
+
+/* compress -> decompress of a host tensor (the reference round trip, acceptance.cpp
+ * criterion 3) with H2D, K1, K2 and D2H pipelined over chunks */
+int taco_roundtrip_host(taco_ctx* ctx, const taco_config* cfg, const void* x_host, int dtype,
+                        uint64_t n, void* out_host, int out_dtype);
+
+/* taco::allreduce(RankSet{TwoShot}) on host buffers: inputs [P][n] f32 -> result[n] f32
+ * (collective.cpp:75-111), computed on the device by taco_allreduce_sim_dev.
+ * stage1_host (optional): P*ceil(n/P) f32 ascending-rank sums before re-encoding. */
+int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* inputs_host,
+                            uint32_t nranks, uint64_t n, float* result_host, float* stage1_host);
+
+/* ---------------------------------------------------------------- diagnostics ------
+ * Element-wise FP8 conversion with exactly the instructions K1/K2/K3 use
+ * (cvt.rn.satfinite.{e4m3,e5m2}x2.f32 / cvt.f16x2.{e4m3,e5m2}x2), replacing
+ * taco::fp8_encode / fp8_decode (fp8.hpp:28-34) for bulk checks on the device. */
+int taco_fp8_encode_dev(const float* x, uint64_t n, int format, uint8_t* out, void* stream);
+int taco_fp8_decode_dev(const uint8_t* codes, uint64_t n, int format, float* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

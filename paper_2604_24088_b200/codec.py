@@ -1,0 +1,209 @@
+"""Torch-facing device API of the TACO codec (K1 / K2 / K3) over the C ABI.
+
+Mirrors the reference's operator API (proj/include/taco/codec.hpp:57-62):
+``compress`` / ``decompress`` keep their names and argument meaning, but take
+and return CUDA tensors and never leave the device.  Messages are uint8 CUDA
+tensors laid out as include/taco_b200.h documents (codes, then (alpha, scale)).
+Errors raise TacoError with the reference's code and message; data-dependent
+ones (NaN/Inf input, bad scalars) are raised when ``check`` synchronises.
+
+torch is plumbing only: device memory, the current stream, dtypes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _abi
+from ._abi import DT_BF16, DT_F32, E4M3, E5M2, Config, TacoError, make_config  # noqa: F401
+
+_DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
+
+
+def _dtype_code(t: torch.dtype) -> int:
+    try:
+        return _DT[t]
+    except KeyError:
+        raise TacoError(_abi.ERR_USAGE, f"unsupported element dtype {t} (float32 or bfloat16)") from None
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _require_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise TacoError(_abi.ERR_USAGE, "tensors must live on a CUDA device (no CPU fallback)")
+
+
+def cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+@dataclass
+class Geometry:
+    """Shard / block / message geometry of one call (collective.cpp:76-87)."""
+
+    n: int
+    shards: int
+    block_size: int
+
+    @property
+    def shard_len(self) -> int:
+        return cdiv(self.n, self.shards)
+
+    @property
+    def blocks(self) -> int:
+        return cdiv(self.shard_len, self.block_size)
+
+    def layout(self, cfg: Config, nblocks: int | None = None) -> _abi.Layout:
+        return _abi.msg_layout(cfg, self.blocks if nblocks is None else nblocks)
+
+
+class Flags:
+    """A device int of error flags (TACO_FLAG_*), checked on demand."""
+
+    def __init__(self, device=None):
+        self.t = torch.zeros(1, dtype=torch.int32, device=device or "cuda")
+
+    def ptr(self):
+        return C.c_void_p(self.t.data_ptr())
+
+    def reset(self):
+        self.t.zero_()
+
+    def check(self):
+        _abi.check(_abi.lib().taco_flags_status(int(self.t.item())))
+
+
+def compress(x: torch.Tensor, cfg: Config, shards: int = 1, blk: tuple[int, int] | None = None,
+             out: torch.Tensor | None = None, flags: Flags | None = None, stream=None) -> torch.Tensor:
+    """K1: taco::compress of a CUDA tensor (flattened), cut into ``shards`` shards.
+
+    Returns a uint8 tensor [shards, msg_stride] (message p = shard p)."""
+    _require_cuda(x)
+    x = x.reshape(-1)
+    if not x.is_contiguous():
+        x = x.contiguous()
+    n = x.numel()
+    g = Geometry(n, shards, cfg.block_size)
+    b0, b1 = blk if blk is not None else (0, g.blocks if n else 0)
+    lay = _abi.msg_layout(cfg, b1 - b0)
+    if out is None:
+        out = torch.empty((shards, lay.msg_stride), dtype=torch.uint8, device=x.device)
+    _require_cuda(out)
+    _abi.check(_abi.lib().taco_compress_dev(C.byref(cfg), _ptr(x), _dtype_code(x.dtype), n, shards, b0, b1,
+                                            _ptr(out), lay.msg_stride, flags.ptr() if flags else None,
+                                            C.c_void_p(_stream(stream))))
+    return out
+
+
+def decompress(msgs: torch.Tensor, n: int, cfg: Config, shards: int = 1, out_dtype=torch.float32,
+               blk: tuple[int, int] | None = None, out: torch.Tensor | None = None,
+               flags: Flags | None = None, stream=None, msg_stride: int | None = None) -> torch.Tensor:
+    """K2: taco::decompress of ``shards`` messages into a flat tensor of n elements."""
+    _require_cuda(msgs)
+    g = Geometry(n, shards, cfg.block_size)
+    b0, b1 = blk if blk is not None else (0, g.blocks if n else 0)
+    stride = msg_stride if msg_stride is not None else _abi.msg_layout(cfg, b1 - b0).msg_stride
+    if out is None:
+        out = torch.empty(n, dtype=out_dtype, device=msgs.device)
+    _require_cuda(out)
+    _abi.check(_abi.lib().taco_decompress_dev(C.byref(cfg), _ptr(msgs), stride, shards, n, b0, b1, _ptr(out),
+                                              _dtype_code(out.dtype), flags.ptr() if flags else None,
+                                              C.c_void_p(_stream(stream))))
+    return out
+
+
+def reduce_encode(msgs: torch.Tensor, nranks: int, shard_len: int, cfg: Config, rank_stride: int,
+                  out_msg: torch.Tensor, acc_out: torch.Tensor | None = None,
+                  blk: tuple[int, int] | None = None, flags: Flags | None = None, stream=None) -> torch.Tensor:
+    """K3: ascending-rank fp32 sum of ``nranks`` decoded messages of one shard, re-encoded.
+
+    ``msgs`` points at rank 0's message; rank r's is ``rank_stride`` bytes further."""
+    _require_cuda(msgs, out_msg, acc_out)
+    m = cdiv(shard_len, cfg.block_size)
+    b0, b1 = blk if blk is not None else (0, m)
+    _abi.check(_abi.lib().taco_reduce_encode_dev(
+        C.byref(cfg), _ptr(msgs), rank_stride, nranks, shard_len, b0, b1, _ptr(out_msg), _ptr(acc_out),
+        _dtype_code(acc_out.dtype) if acc_out is not None else DT_F32, flags.ptr() if flags else None,
+        C.c_void_p(_stream(stream))))
+    return out_msg
+
+
+def allreduce_sim(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float32, stage1: torch.Tensor | None = None,
+                  flags: Flags | None = None, stream=None) -> torch.Tensor:
+    """taco::allreduce(RankSet{TwoShot}) with all P ranks on this device: inputs [P, n]."""
+    _require_cuda(inputs, stage1)
+    p, n = inputs.shape
+    inputs = inputs.contiguous()
+    ws = torch.empty(max(1, _abi.lib().taco_allreduce_sim_workspace(C.byref(cfg), p, n)), dtype=torch.uint8,
+                     device=inputs.device)
+    out = torch.empty(n, dtype=out_dtype, device=inputs.device)
+    _abi.check(_abi.lib().taco_allreduce_sim_dev(C.byref(cfg), _ptr(inputs), _dtype_code(inputs.dtype), p, n,
+                                                 _ptr(out), _dtype_code(out_dtype), _ptr(stage1), _ptr(ws),
+                                                 flags.ptr() if flags else None, C.c_void_p(_stream(stream))))
+    return out
+
+
+def split_message(msg: torch.Tensor, cfg: Config, nblocks: int):
+    """(codes [nblocks*B] uint8, alpha [nblocks] f32, scale [nblocks] f32) views of one message."""
+    lay = _abi.msg_layout(cfg, nblocks)
+    codes = msg[: lay.codes_bytes]
+    scal = msg[lay.scal_offset: lay.scal_offset + 8 * nblocks].view(torch.float32).view(nblocks, 2)
+    return codes, scal[:, 0], scal[:, 1]
+
+
+class HostContext:
+    """taco_ctx: synchronous host-buffer API (the shape of the reference's calls)."""
+
+    def __init__(self, device: int = 0):
+        h = C.c_void_p()
+        _abi.check(_abi.lib().taco_ctx_create(device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if self.h:
+            _abi.lib().taco_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def roundtrip(self, x: torch.Tensor, cfg: Config, out: torch.Tensor) -> torch.Tensor:
+        """compress -> decompress of a host tensor; out is a host tensor of x's size."""
+        _abi.check(_abi.lib().taco_roundtrip_host(self.h, C.byref(cfg), _ptr(x), _dtype_code(x.dtype), x.numel(),
+                                                  _ptr(out), _dtype_code(out.dtype)))
+        return out
+
+    def compress(self, x: torch.Tensor, cfg: Config) -> torch.Tensor:
+        m = cdiv(x.numel(), cfg.block_size)
+        msg = torch.empty(_abi.msg_layout(cfg, m).msg_bytes, dtype=torch.uint8)
+        _abi.check(_abi.lib().taco_compress_host(self.h, C.byref(cfg), _ptr(x), _dtype_code(x.dtype), x.numel(),
+                                                 _ptr(msg)))
+        return msg
+
+    def decompress(self, msg: torch.Tensor, n: int, cfg: Config, out_dtype=torch.float32) -> torch.Tensor:
+        out = torch.empty(n, dtype=out_dtype)
+        _abi.check(_abi.lib().taco_decompress_host(self.h, C.byref(cfg), _ptr(msg), n, _ptr(out),
+                                                   _dtype_code(out_dtype)))
+        return out
+
+    def allreduce_sim(self, inputs: torch.Tensor, cfg: Config, want_stage1: bool = False):
+        p, n = inputs.shape
+        res = torch.empty(n, dtype=torch.float32)
+        st = torch.empty(p * cdiv(n, p), dtype=torch.float32) if want_stage1 else None
+        _abi.check(_abi.lib().taco_allreduce_sim_host(self.h, C.byref(cfg), _ptr(inputs.contiguous()), p, n,
+                                                      _ptr(res), _ptr(st)))
+        return (res, st) if want_stage1 else res

@@ -1,0 +1,46 @@
+// K1 dispatch: block size x input dtype x FP8 format.
+#include "taco_kernels.cuh"
+#include "taco_launch.h"
+
+namespace taco_impl {
+using namespace taco_dev;
+
+namespace {
+template <int B, typename T, int FMT>
+cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    const uint64_t jobs = (uint64_t)a.P * a.nblk;
+    if (jobs == 0) return cudaSuccess;
+    if constexpr (B <= 1024) {
+        constexpr int VMAX = 16 / (int)sizeof(T);
+        using Gm = Geo<B, 32, VMAX>;
+        k_compress<B, T, FMT, 32, VMAX><<<warp_grid(jobs, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
+            static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c);
+    } else {
+        const size_t smem = (size_t)B * sizeof(float);
+        auto* kern = &k_compress_big<B, T, FMT>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)jobs, kBigThreads, smem, l.stream>>>(static_cast<const T*>(l.in),
+                                                              static_cast<uint8_t*>(l.out), a, c);
+    }
+    return cudaGetLastError();
+}
+
+template <typename T, int FMT>
+cudaError_t by_size(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    switch (l.block_size) {
+#define CASE(B) \
+    case B: return run<B, T, FMT>(l, a, c);
+        TACO_WARP_SIZES(CASE)
+        TACO_BIG_SIZES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+}  // namespace
+
+cudaError_t launch_compress(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    if (l.dtype == 1) return l.format ? by_size<__nv_bfloat16, 1>(l, a, c) : by_size<__nv_bfloat16, 0>(l, a, c);
+    return l.format ? by_size<float, 1>(l, a, c) : by_size<float, 0>(l, a, c);
+}
+
+}  // namespace taco_impl

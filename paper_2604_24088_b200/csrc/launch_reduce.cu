@@ -1,0 +1,46 @@
+// K3 dispatch: block size x stage-1 output dtype x FP8 format.
+#include "taco_kernels.cuh"
+#include "taco_launch.h"
+
+namespace taco_impl {
+using namespace taco_dev;
+
+namespace {
+template <int B, typename T, int FMT>
+cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    if (a.nblk == 0) return cudaSuccess;
+    if constexpr (B <= 1024) {
+        using Gm = Geo<B, 32, 8>;
+        k_reduce_encode<B, T, FMT, 32, 8><<<warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
+            static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
+    } else {
+        const size_t smem = (size_t)B * sizeof(float);
+        auto* kern = &k_reduce_encode_big<B, T, FMT>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<(unsigned)a.nblk, kBigThreads, smem, l.stream>>>(static_cast<const uint8_t*>(l.in),
+                                                                static_cast<uint8_t*>(l.out),
+                                                                static_cast<T*>(l.acc), a, c);
+    }
+    return cudaGetLastError();
+}
+
+template <typename T, int FMT>
+cudaError_t by_size(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    switch (l.block_size) {
+#define CASE(B) \
+    case B: return run<B, T, FMT>(l, a, c);
+        TACO_WARP_SIZES(CASE)
+        TACO_BIG_SIZES(CASE)
+#undef CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+}  // namespace
+
+cudaError_t launch_reduce_encode(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    if (l.acc && l.dtype == 1)
+        return l.format ? by_size<__nv_bfloat16, 1>(l, a, c) : by_size<__nv_bfloat16, 0>(l, a, c);
+    return l.format ? by_size<float, 1>(l, a, c) : by_size<float, 0>(l, a, c);
+}
+
+}  // namespace taco_impl

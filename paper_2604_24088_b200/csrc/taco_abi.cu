@@ -1,0 +1,543 @@
+// taco_abi.cu -- the extern "C" boundary (include/taco_b200.h): validation with the
+// reference's exact messages, shard/message geometry, kernel launches, the one-device
+// RankSet simulation and the pipelined host API.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "taco_b200.h"
+#include "taco_kernels.cuh"
+#include "taco_launch.h"
+
+using taco_dev::CodecConsts;
+using taco_dev::ShardArgs;
+using taco_impl::Launch;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+    return fail(TACO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define TACO_CUDA(call)                                        \
+    do {                                                       \
+        cudaError_t e_ = (call);                               \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
+    } while (0)
+
+bool pow2(uint64_t b) { return b != 0 && (b & (b - 1)) == 0; }
+
+uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
+
+size_t dtype_size(int dt) { return dt == TACO_DT_BF16 ? 2 : 4; }
+
+// transform.cpp:13-20, codec.cpp:189-197 -- same order, same messages
+int check_config(const taco_config* cfg) {
+    if (!cfg) return fail(TACO_ERR_USAGE, "null codec config");
+    const uint64_t b = cfg->block_size;
+    if (!pow2(b)) return fail(TACO_ERR_CONFIG, "block size must be a power of two");
+    if (b < 2 || b > 32768) return fail(TACO_ERR_CONFIG, "block size must be between 2 and 32768");
+    if (!(cfg->target_energy > 0.0f) || !std::isfinite(cfg->target_energy))
+        return fail(TACO_ERR_CONFIG, "target energy must be positive and finite");
+    if (!(cfg->stability_epsilon > 0.0f) || !std::isfinite(cfg->stability_epsilon))
+        return fail(TACO_ERR_CONFIG, "stability epsilon must be positive and finite");
+    if (cfg->format > 1) return fail(TACO_ERR_CONFIG, "unknown fp8 format");
+    if (cfg->kind != 0)
+        return fail(TACO_ERR_CONFIG, "only CodecKind::Taco is implemented on the device path");
+    return TACO_OK;
+}
+
+int check_dtype(int dt) {
+    if (dt != TACO_DT_F32 && dt != TACO_DT_BF16) return fail(TACO_ERR_USAGE, "unknown element dtype");
+    return TACO_OK;
+}
+
+CodecConsts consts_of(const taco_config* cfg) {
+    CodecConsts c;
+    c.tau = cfg->target_energy;
+    c.eps = cfg->stability_epsilon;
+    c.inv_b = 1.0 / (double)cfg->block_size;
+    c.norm = 1.0 / std::sqrt((double)cfg->block_size);  // transform.cpp:56
+    c.qmax = cfg->format ? 57344.0 : 448.0;             // fp8.cpp:11-12
+    return c;
+}
+
+taco_layout layout_of(uint64_t b, uint64_t nblocks) {
+    taco_layout l;
+    l.nblocks = nblocks;
+    l.codes_bytes = nblocks * b;
+    l.scal_offset = align16(l.codes_bytes);
+    l.msg_bytes = l.scal_offset + 8 * nblocks;
+    l.msg_stride = align16(l.msg_bytes);
+    return l;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
+    if (blk_begin > blk_end || blk_end > m)
+        return fail(TACO_ERR_USAGE, "block range exceeds the shard's block count");
+    return TACO_OK;
+}
+
+}  // namespace
+
+// =================================================================== metadata ====
+extern "C" {
+
+int taco_abi_version(void) { return TACO_B200_ABI_VERSION; }
+
+const char* taco_last_error(void) { return g_err.c_str(); }
+
+taco_config taco_default_config(void) {
+    taco_config c;
+    c.block_size = 256;
+    c.target_energy = 1.0f;
+    c.stability_epsilon = 1e-12f;
+    c.format = 0;
+    c.kind = 0;
+    return c;
+}
+
+int taco_validate_config(const taco_config* cfg) { return check_config(cfg); }
+
+int taco_msg_layout(const taco_config* cfg, uint64_t nblocks, taco_layout* out) {
+    if (int rc = check_config(cfg)) return rc;
+    *out = layout_of(cfg->block_size, nblocks);
+    return TACO_OK;
+}
+
+double taco_compressed_ratio(const taco_config* cfg, uint64_t n) {
+    if (n == 0 || !cfg) return 0.0;
+    const double blocks = (double)div_up(n, cfg->block_size);
+    return 4.0 * (double)n / (blocks * ((double)cfg->block_size + 8.0));  // codec.cpp:298-304
+}
+
+uint64_t taco_archive_size(const taco_config* cfg, uint64_t n) {
+    return 22 + div_up(n, cfg->block_size) * ((uint64_t)cfg->block_size + 8);  // serialize.cpp:172-177
+}
+
+int taco_flags_status(int flags) {
+    if (flags & TACO_FLAG_NONFINITE_INPUT) return fail(TACO_ERR_INPUT, "input tensor contains NaN or Inf");
+    if (flags & TACO_FLAG_BAD_SCALARS) return fail(TACO_ERR_CORRUPT, "block scalars must be finite and nonzero");
+    return TACO_OK;
+}
+
+// ================================================================= device API ====
+
+int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, uint32_t shards,
+                      uint64_t blk_begin, uint64_t blk_end, void* msgs, uint64_t msg_stride, int* d_flags,
+                      void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (shards == 0) return fail(TACO_ERR_USAGE, "shard count must be positive");
+    const uint64_t b = cfg->block_size, S = div_up(n, shards), m = div_up(S, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
+                aligned16(x) && (shards == 1 || S % 8 == 0), d_flags};
+    Launch l{cfg->block_size, dtype, (int)cfg->format, x, msgs, nullptr, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_compress(l, a, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    return TACO_OK;
+}
+
+int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_stride, uint32_t shards, uint64_t n,
+                        uint64_t blk_begin, uint64_t blk_end, void* out, int out_dtype, int* d_flags, void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (int rc = check_dtype(out_dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_CORRUPT, "compressed tensor declares zero elements");
+    if (shards == 0) return fail(TACO_ERR_USAGE, "shard count must be positive");
+    const uint64_t b = cfg->block_size, S = div_up(n, shards), m = div_up(S, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
+                aligned16(out) && (shards == 1 || S % 8 == 0), d_flags};
+    Launch l{cfg->block_size, out_dtype, (int)cfg->format, msgs, out, nullptr, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_decompress(l, a, consts_of(cfg)))
+        return cuda_fail(e, "K2 decompress launch");
+    return TACO_OK;
+}
+
+int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride, uint32_t nranks,
+                           uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end, void* out_msg, void* acc_out,
+                           int acc_dtype, int* d_flags, void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (acc_out)
+        if (int rc = check_dtype(acc_dtype)) return rc;
+    if (nranks == 0) return fail(TACO_ERR_USAGE, "reduction needs at least one rank");
+    if (shard_len == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint64_t b = cfg->block_size, m = div_up(shard_len, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (nranks > 1 && rank_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
+                acc_out ? aligned16(acc_out) : 0, d_flags};
+    Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, out_msg, acc_out, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
+        return cuda_fail(e, "K3 reduce-encode launch");
+    return TACO_OK;
+}
+
+uint64_t taco_allreduce_sim_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n) {
+    if (!cfg || nranks == 0 || n == 0) return 0;
+    const uint64_t S = div_up(n, nranks);
+    const taco_layout lay = layout_of(cfg->block_size, div_up(S, cfg->block_size));
+    // phase-1 messages [rank][shard] + re-encoded shards [shard]
+    return (uint64_t)nranks * nranks * lay.msg_stride + (uint64_t)nranks * lay.msg_stride;
+}
+
+// collective.cpp:75-111 on one device: K1 per rank into its P shard messages, K3 per
+// shard over the P ranks' messages (ascending), K2 of the P re-encoded shards.
+int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype, uint32_t nranks, uint64_t n,
+                           void* out, int out_dtype, float* stage1, void* work, int* d_flags, void* stream) {
+    if (nranks < 2) return fail(TACO_ERR_USAGE, "allreduce needs at least 2 ranks");
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (int rc = check_config(cfg)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    const uint64_t P = nranks, S = div_up(n, P), m = div_up(S, cfg->block_size);
+    const taco_layout lay = layout_of(cfg->block_size, m);
+    uint8_t* sent = static_cast<uint8_t*>(work);
+    uint8_t* reduced = sent + P * P * lay.msg_stride;
+    const uint8_t* in = static_cast<const uint8_t*>(inputs);
+    for (uint64_t r = 0; r < P; ++r) {
+        if (int rc = taco_compress_dev(cfg, in + r * n * dtype_size(dtype), dtype, n, nranks, 0, m,
+                                       sent + r * P * lay.msg_stride, lay.msg_stride, d_flags, stream))
+            return rc;
+    }
+    for (uint64_t s = 0; s < P; ++s) {
+        if (int rc = taco_reduce_encode_dev(cfg, sent + s * lay.msg_stride, P * lay.msg_stride, nranks, S, 0, m,
+                                            reduced + s * lay.msg_stride, stage1 ? stage1 + s * S : nullptr,
+                                            TACO_DT_F32, d_flags, stream))
+            return rc;
+    }
+    return taco_decompress_dev(cfg, reduced, lay.msg_stride, nranks, n, 0, m, out, out_dtype, d_flags, stream);
+}
+
+}  // extern "C"
+
+// =================================================================== host API ====
+// Pipelined host <-> device path.  Chunks of whole blocks rotate over kSlots streams;
+// each slot has its own device buffers, so chunk i's H2D, kernels and D2H overlap
+// with its neighbours' (two copy engines + SMs).  Pageable user memory is staged
+// through pinned slot buffers; pinned user memory is copied directly.
+
+struct taco_ctx {
+    static constexpr int kSlots = 3;
+    int device = 0;
+    cudaStream_t st[kSlots] = {};
+    void* d_in[kSlots] = {};
+    void* d_msg[kSlots] = {};
+    void* d_out[kSlots] = {};
+    int* d_flags = nullptr;
+    size_t cap_in = 0, cap_msg = 0, cap_out = 0;
+    void* h_stage_in[kSlots] = {};
+    void* h_stage_out[kSlots] = {};
+    size_t cap_stage_in = 0, cap_stage_out = 0;
+    std::mutex mu;
+};
+
+namespace {
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+int grow_dev(void** bufs, size_t& cap, size_t need) {
+    if (need <= cap) return TACO_OK;
+    for (int i = 0; i < taco_ctx::kSlots; ++i) {
+        if (bufs[i]) cudaFree(bufs[i]);
+        bufs[i] = nullptr;
+        TACO_CUDA(cudaMalloc(&bufs[i], need));
+    }
+    cap = need;
+    return TACO_OK;
+}
+
+int grow_host(void** bufs, size_t& cap, size_t need) {
+    if (need <= cap) return TACO_OK;
+    for (int i = 0; i < taco_ctx::kSlots; ++i) {
+        if (bufs[i]) cudaFreeHost(bufs[i]);
+        bufs[i] = nullptr;
+        TACO_CUDA(cudaMallocHost(&bufs[i], need));
+    }
+    cap = need;
+    return TACO_OK;
+}
+
+// chunk = whole blocks, ~8 MiB of input per chunk
+uint64_t chunk_blocks(uint64_t b, size_t elt) {
+    const uint64_t target = (8ull << 20) / elt;
+    return std::max<uint64_t>(1, target / b);
+}
+
+int finish(taco_ctx* ctx) {
+    for (int i = 0; i < taco_ctx::kSlots; ++i) TACO_CUDA(cudaStreamSynchronize(ctx->st[i]));
+    int flags = 0;
+    TACO_CUDA(cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+    return taco_flags_status(flags);
+}
+
+}  // namespace
+
+extern "C" {
+
+int taco_ctx_create(int device, taco_ctx** out) {
+    auto* c = new taco_ctx();
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    for (int i = 0; i < taco_ctx::kSlots && e == cudaSuccess; ++i)
+        e = cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_flags, sizeof(int));
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "taco_ctx_create");
+    }
+    *out = c;
+    return TACO_OK;
+}
+
+void taco_ctx_destroy(taco_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    for (int i = 0; i < taco_ctx::kSlots; ++i) {
+        if (c->st[i]) cudaStreamSynchronize(c->st[i]);
+        cudaFree(c->d_in[i]);
+        cudaFree(c->d_msg[i]);
+        cudaFree(c->d_out[i]);
+        if (c->h_stage_in[i]) cudaFreeHost(c->h_stage_in[i]);
+        if (c->h_stage_out[i]) cudaFreeHost(c->h_stage_out[i]);
+        if (c->st[i]) cudaStreamDestroy(c->st[i]);
+    }
+    cudaFree(c->d_flags);
+    delete c;
+}
+
+// Shared driver of the three host calls.  mode 0 = compress, 1 = decompress, 2 = round trip.
+static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const void* src, int in_dtype,
+                         uint64_t n, void* dst, int out_dtype) {
+    if (!ctx) return fail(TACO_ERR_USAGE, "null taco context");
+    if (int rc = check_config(cfg)) return rc;
+    if (mode != 1)
+        if (int rc = check_dtype(in_dtype)) return rc;
+    if (mode != 0)
+        if (int rc = check_dtype(out_dtype)) return rc;
+    if (n == 0) return mode == 1 ? fail(TACO_ERR_CORRUPT, "compressed tensor declares zero elements")
+                                 : fail(TACO_ERR_INPUT, "input tensor is empty");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    TACO_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t b = cfg->block_size, m = div_up(n, b);
+    const size_t ein = mode == 1 ? 1 : dtype_size(in_dtype);
+    const size_t eout = mode == 0 ? 1 : dtype_size(out_dtype);
+    const uint64_t cb = chunk_blocks(b, mode == 1 ? 4 : ein);
+    const taco_layout full = layout_of(b, m);
+    const taco_layout cl = layout_of(b, std::min(cb, m));
+    const size_t in_bytes = mode == 1 ? cl.msg_stride : cb * b * ein;
+    const size_t out_bytes = mode == 0 ? cl.msg_stride : cb * b * eout;
+    if (int rc = grow_dev(ctx->d_in, ctx->cap_in, in_bytes)) return rc;
+    if (int rc = grow_dev(ctx->d_msg, ctx->cap_msg, cl.msg_stride)) return rc;
+    if (int rc = grow_dev(ctx->d_out, ctx->cap_out, out_bytes)) return rc;
+    const bool pin_in = is_pinned(src), pin_out = is_pinned(dst);
+    if (!pin_in)
+        if (int rc = grow_host(ctx->h_stage_in, ctx->cap_stage_in, in_bytes)) return rc;
+    if (!pin_out)
+        if (int rc = grow_host(ctx->h_stage_out, ctx->cap_stage_out, out_bytes)) return rc;
+    TACO_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->st[0]));
+    TACO_CUDA(cudaStreamSynchronize(ctx->st[0]));
+
+    const uint8_t* s8 = static_cast<const uint8_t*>(src);
+    uint8_t* d8 = static_cast<uint8_t*>(dst);
+    const uint64_t nchunks = div_up(m, cb);
+    // staged output copies still in flight per slot: (host dst, bytes) pairs
+    std::vector<std::pair<uint8_t*, size_t>> pending[taco_ctx::kSlots];
+    auto drain = [&](int slot) -> int {
+        if (pin_out || pending[slot].empty()) return TACO_OK;
+        TACO_CUDA(cudaStreamSynchronize(ctx->st[slot]));
+        size_t off = 0;
+        for (auto& pr : pending[slot]) {
+            std::memcpy(pr.first, static_cast<uint8_t*>(ctx->h_stage_out[slot]) + off, pr.second);
+            off += pr.second;
+        }
+        pending[slot].clear();
+        return TACO_OK;
+    };
+    for (uint64_t ci = 0; ci < nchunks; ++ci) {
+        const int slot = (int)(ci % taco_ctx::kSlots);
+        cudaStream_t st = ctx->st[slot];
+        const uint64_t b0 = ci * cb, b1 = std::min(m, b0 + cb), nb = b1 - b0;
+        const uint64_t e0 = b0 * b, e1 = std::min<uint64_t>(n, b1 * b), ne = e1 - e0;
+        const taco_layout lay = layout_of(b, nb);
+        if (int rc = drain(slot)) return rc;  // slot buffers free again
+        if (!pin_in) TACO_CUDA(cudaStreamSynchronize(st));
+        // ---- H2D
+        auto h2d = [&](void* d, const uint8_t* h, size_t bytes, size_t stage_off) -> int {
+            if (pin_in) {
+                TACO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+            } else {
+                uint8_t* stage = static_cast<uint8_t*>(ctx->h_stage_in[slot]) + stage_off;
+                std::memcpy(stage, h, bytes);
+                TACO_CUDA(cudaMemcpyAsync(d, stage, bytes, cudaMemcpyHostToDevice, st));
+            }
+            return TACO_OK;
+        };
+        if (mode == 1) {  // chunk of the full message -> chunk message layout
+            uint8_t* d = static_cast<uint8_t*>(ctx->d_in[slot]);
+            if (int rc = h2d(d, s8 + b0 * b, nb * b, 0)) return rc;
+            if (int rc = h2d(d + lay.scal_offset, s8 + full.scal_offset + b0 * 8, nb * 8, lay.scal_offset)) return rc;
+        } else {
+            if (int rc = h2d(ctx->d_in[slot], s8 + e0 * ein, ne * ein, 0)) return rc;
+        }
+        // ---- kernels (the chunk is a standalone tensor of ne elements: blocks never span chunks)
+        void* msg = mode == 1 ? ctx->d_in[slot] : (mode == 0 ? ctx->d_out[slot] : ctx->d_msg[slot]);
+        if (mode != 1)
+            if (int rc = taco_compress_dev(cfg, ctx->d_in[slot], in_dtype, ne, 1, 0, nb, msg, lay.msg_stride,
+                                           ctx->d_flags, st))
+                return rc;
+        if (mode != 0)
+            if (int rc = taco_decompress_dev(cfg, msg, lay.msg_stride, 1, ne, 0, nb, ctx->d_out[slot], out_dtype,
+                                             ctx->d_flags, st))
+                return rc;
+        // ---- D2H
+        auto d2h = [&](uint8_t* h, const void* d, size_t bytes, size_t stage_off) -> int {
+            if (pin_out) {
+                TACO_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+            } else {
+                uint8_t* stage = static_cast<uint8_t*>(ctx->h_stage_out[slot]) + stage_off;
+                TACO_CUDA(cudaMemcpyAsync(stage, d, bytes, cudaMemcpyDeviceToHost, st));
+                pending[slot].push_back({h, bytes});
+            }
+            return TACO_OK;
+        };
+        if (mode == 0) {
+            const uint8_t* d = static_cast<const uint8_t*>(ctx->d_out[slot]);
+            if (int rc = d2h(d8 + b0 * b, d, nb * b, 0)) return rc;
+            if (int rc = d2h(d8 + full.scal_offset + b0 * 8, d + lay.scal_offset, nb * 8, nb * b)) return rc;
+        } else {
+            if (int rc = d2h(d8 + e0 * eout, ctx->d_out[slot], ne * eout, 0)) return rc;
+        }
+    }
+    for (int i = 0; i < taco_ctx::kSlots; ++i)
+        if (int rc = drain(i)) return rc;
+    return finish(ctx);
+}
+
+int taco_compress_host(taco_ctx* ctx, const taco_config* cfg, const void* x_host, int dtype, uint64_t n,
+                       void* msg_host) {
+    return host_pipeline(ctx, cfg, 0, x_host, dtype, n, msg_host, 0);
+}
+
+int taco_decompress_host(taco_ctx* ctx, const taco_config* cfg, const void* msg_host, uint64_t n, void* out_host,
+                         int out_dtype) {
+    return host_pipeline(ctx, cfg, 1, msg_host, 0, n, out_host, out_dtype);
+}
+
+int taco_roundtrip_host(taco_ctx* ctx, const taco_config* cfg, const void* x_host, int dtype, uint64_t n,
+                        void* out_host, int out_dtype) {
+    return host_pipeline(ctx, cfg, 2, x_host, dtype, n, out_host, out_dtype);
+}
+
+int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* inputs_host, uint32_t nranks,
+                            uint64_t n, float* result_host, float* stage1_host) {
+    if (!ctx) return fail(TACO_ERR_USAGE, "null taco context");
+    if (nranks < 2) return fail(TACO_ERR_USAGE, "allreduce needs at least 2 ranks");
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (int rc = check_config(cfg)) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    TACO_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t S = div_up(n, nranks);
+    const size_t in_bytes = (size_t)nranks * n * 4, st_bytes = stage1_host ? (size_t)nranks * S * 4 : 0;
+    const size_t ws = taco_allreduce_sim_workspace(cfg, nranks, n);
+    void *d_in = nullptr, *d_out = nullptr, *d_st = nullptr, *d_ws = nullptr;
+    cudaStream_t st = ctx->st[0];
+    int rc = TACO_OK;
+    cudaError_t e = cudaMalloc(&d_in, in_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&d_out, n * 4);
+    if (e == cudaSuccess && st_bytes) e = cudaMalloc(&d_st, st_bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&d_ws, ws);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, inputs_host, in_bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "allreduce staging");
+    if (rc == TACO_OK)
+        rc = taco_allreduce_sim_dev(cfg, d_in, TACO_DT_F32, nranks, n, d_out, TACO_DT_F32,
+                                    static_cast<float*>(d_st), d_ws, ctx->d_flags, st);
+    if (rc == TACO_OK) {
+        e = cudaMemcpyAsync(result_host, d_out, n * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && st_bytes) e = cudaMemcpyAsync(stage1_host, d_st, st_bytes, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "allreduce readback");
+    }
+    if (rc == TACO_OK) {
+        int flags = 0;
+        e = cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
+        rc = e != cudaSuccess ? cuda_fail(e, "flags readback") : taco_flags_status(flags);
+    }
+    cudaFree(d_in);
+    cudaFree(d_out);
+    cudaFree(d_st);
+    cudaFree(d_ws);
+    return rc;
+}
+
+}  // extern "C"
+
+// ============================================================= diagnostics ====
+// Element-wise access to the exact FP8 conversion instructions the kernels use
+// (enc2 / dec2 in taco_device.cuh), so tests can prove them equal to the reference's
+// fp8_encode / decode table (fp8.cpp:16-91) over every fp32 bit pattern.
+namespace {
+template <int FMT>
+__global__ void k_fp8_encode(const float* __restrict__ x, uint64_t n, uint8_t* __restrict__ out) {
+    const uint64_t i = 2 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (i + 1 < n) {
+        *reinterpret_cast<uint16_t*>(out + i) = (uint16_t)taco_dev::enc2<FMT>(x[i], x[i + 1]);
+    } else if (i < n) {
+        out[i] = (uint8_t)taco_dev::enc2<FMT>(x[i], 0.0f);
+    }
+}
+template <int FMT>
+__global__ void k_fp8_decode(const uint8_t* __restrict__ c, uint64_t n, float* __restrict__ out) {
+    const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        float lo, hi;
+        taco_dev::dec2<FMT>(c[i], lo, hi);
+        out[i] = lo;
+    }
+}
+}  // namespace
+
+extern "C" int taco_fp8_encode_dev(const float* x, uint64_t n, int format, uint8_t* out, void* stream) {
+    if (n == 0) return TACO_OK;
+    const unsigned grid = (unsigned)div_up(div_up(n, 2), 256);
+    if (format) k_fp8_encode<1><<<grid, 256, 0, (cudaStream_t)stream>>>(x, n, out);
+    else k_fp8_encode<0><<<grid, 256, 0, (cudaStream_t)stream>>>(x, n, out);
+    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "fp8 encode launch");
+    return TACO_OK;
+}
+
+extern "C" int taco_fp8_decode_dev(const uint8_t* codes, uint64_t n, int format, float* out, void* stream) {
+    if (n == 0) return TACO_OK;
+    const unsigned grid = (unsigned)div_up(n, 256);
+    if (format) k_fp8_decode<1><<<grid, 256, 0, (cudaStream_t)stream>>>(codes, n, out);
+    else k_fp8_decode<0><<<grid, 256, 0, (cudaStream_t)stream>>>(codes, n, out);
+    if (cudaError_t e = cudaGetLastError()) return cuda_fail(e, "fp8 decode launch");
+    return TACO_OK;
+}

@@ -1,0 +1,40 @@
+// taco_launch.h -- host-side launch descriptors shared by the kernel dispatch units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace taco_dev {
+struct ShardArgs;
+struct CodecConsts;
+}  // namespace taco_dev
+
+namespace taco_impl {
+
+// One kernel launch: B, element dtype (0 f32, 1 bf16), FP8 format, pointers.
+struct Launch {
+    uint32_t block_size;
+    int dtype;   // K1: input, K2: output, K3: acc_out (ignored when acc == nullptr)
+    int format;  // 0 E4M3, 1 E5M2
+    const void* in;
+    void* out;
+    void* acc;   // K3 only
+    cudaStream_t stream;
+};
+
+cudaError_t launch_compress(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
+cudaError_t launch_decompress(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
+cudaError_t launch_reduce_encode(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
+
+// grid for the warp kernels: one L-lane group per block job
+inline unsigned warp_grid(uint64_t jobs, int blocks_per_warp, int threads) {
+    const uint64_t warps = (jobs + blocks_per_warp - 1) / blocks_per_warp;
+    const uint64_t wpc = threads / 32;
+    return (unsigned)((warps + wpc - 1) / wpc);
+}
+
+}  // namespace taco_impl
+
+// Instantiate `MACRO(B)` for every supported block size.
+#define TACO_WARP_SIZES(M) M(2) M(4) M(8) M(16) M(32) M(64) M(128) M(256) M(512) M(1024)
+#define TACO_BIG_SIZES(M) M(2048) M(4096) M(8192) M(16384) M(32768)

@@ -1,0 +1,58 @@
+"""Parity metrics shared by the GPU tests (test infrastructure).
+
+Tolerances are the north-star bounds (BASELINE.json) as calibrated in SURVEY.md §8c:
+  * alpha: bit-exact (fp64 sum of squares);
+  * scale: <= 1e-6 relative;
+  * codes: identical except one-ulp flips (0x00 == 0x80), flip rate <= FLIP_RATE_MAX;
+  * decoded outputs: relMSE vs the oracle <= 1e-6 per round trip, <= 1e-5 end-to-end collectives.
+"""
+import numpy as np
+import torch
+
+FLIP_RATE_MAX = 1e-4
+SCALE_RTOL = 1e-6
+DECODE_RELMSE_MAX = 1e-6
+COLLECTIVE_RELMSE_MAX = 1e-5
+
+
+def code_index(c: np.ndarray) -> np.ndarray:
+    """Signed position of an FP8 code on its (monotone) value grid; 0x00 and 0x80 -> 0."""
+    c = c.astype(np.int32)
+    mag = c & 0x7F
+    return np.where(c & 0x80, -mag, mag)
+
+
+def code_diff(got: np.ndarray, want: np.ndarray):
+    """(number of flipped codes, max ulp distance)."""
+    d = np.abs(code_index(got) - code_index(want))
+    return int(np.count_nonzero(d)), int(d.max()) if d.size else 0
+
+
+def rel_mse(got, want) -> float:
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    den = float(np.sum(want * want))
+    num = float(np.sum((got - want) ** 2))
+    return num / den if den > 0 else num
+
+
+def rel_l2(got, want) -> float:
+    return float(np.sqrt(rel_mse(got, want)))
+
+
+def to_bf16_f32(x: np.ndarray) -> np.ndarray:
+    """float(bf16(x)) with round-to-nearest-even, the exact values a bf16 tensor holds."""
+    return torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def check_codec_parity(codes, alpha, scale, rcodes, ralpha, rscale, what=""):
+    """Stage-isolated K1 parity vs the oracle on the same input; returns the flip rate."""
+    assert np.array_equal(alpha, ralpha), f"{what}: alpha not bit-exact " \
+        f"({np.count_nonzero(alpha != ralpha)} of {alpha.size} differ)"
+    err = np.max(np.abs(scale.astype(np.float64) / rscale - 1.0)) if scale.size else 0.0
+    assert err <= SCALE_RTOL, f"{what}: scale rel err {err}"
+    flips, worst = code_diff(codes, rcodes)
+    assert worst <= 1, f"{what}: a code is {worst} ulps away"
+    rate = flips / max(1, codes.size)
+    assert rate <= FLIP_RATE_MAX, f"{what}: flip rate {rate}"
+    return rate

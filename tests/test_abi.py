@@ -1,0 +1,110 @@
+"""CPU checks of the drop-in boundary: the C-ABI library loads, exports every symbol the
+header declares, and its host-side logic (validation messages, geometry, byte accounting)
+matches the reference -- no kernel launches."""
+import ctypes as C
+import subprocess
+
+import pytest
+
+from paper_2604_24088_b200 import _abi
+from paper_2604_24088_b200._abi import TacoError, make_config
+
+
+def test_library_exports_every_header_symbol():
+    lib = _abi.lib()
+    syms = _abi.header_symbols()
+    assert len(syms) >= 18
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+    out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    assert set(syms) <= exported
+    assert lib.taco_abi_version() == 1
+
+
+def test_default_config_matches_reference_defaults():
+    # codec.hpp:24-33: B=256, tau=1, eps=1e-12, E4M3, Taco
+    c = _abi.lib().taco_default_config()
+    assert (c.block_size, c.target_energy, c.format, c.kind) == (256, 1.0, 0, 0)
+    assert c.stability_epsilon == pytest.approx(1e-12, rel=1e-6)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(block_size=100), "block size must be a power of two"),
+    (dict(block_size=0), "block size must be a power of two"),
+    (dict(block_size=1), "block size must be between 2 and 32768"),
+    (dict(block_size=65536), "block size must be between 2 and 32768"),
+    (dict(target_energy=0.0), "target energy must be positive and finite"),
+    (dict(target_energy=float("inf")), "target energy must be positive and finite"),
+    (dict(stability_epsilon=0.0), "stability epsilon must be positive and finite"),
+    (dict(stability_epsilon=float("nan")), "stability epsilon must be positive and finite"),
+])
+def test_validation_messages_match_reference(kw, msg, port):
+    # codec.cpp:189-197, transform.cpp:13-20 (test_codec.cpp:318-349)
+    cfg = make_config(**kw)
+    with pytest.raises(TacoError, match=msg) as ei:
+        _abi.check(_abi.lib().taco_validate_config(C.byref(cfg)))
+    assert ei.value.code == "config"
+    # and the oracle raises the same message for the same config
+    from oracle.oracle import OracleError
+    with pytest.raises(OracleError, match=msg):
+        port.compress([1.0], block_size=kw.get("block_size", 256), tau=kw.get("target_energy", 1.0),
+                      eps=kw.get("stability_epsilon", 1e-12))
+
+
+def test_empty_input_rejected_before_any_launch():
+    cfg = make_config()
+    with pytest.raises(TacoError, match="input tensor is empty") as ei:
+        _abi.check(_abi.lib().taco_compress_dev(C.byref(cfg), None, 0, 0, 1, 0, 0, None, 0, None, None))
+    assert ei.value.code == "input"
+    with pytest.raises(TacoError, match="compressed tensor declares zero elements") as ei:
+        _abi.check(_abi.lib().taco_decompress_dev(C.byref(cfg), None, 0, 1, 0, 0, 0, None, 0, None, None))
+    assert ei.value.code == "corrupt"
+
+
+def test_allreduce_needs_two_ranks():
+    cfg = make_config()
+    with pytest.raises(TacoError, match="allreduce needs at least 2 ranks") as ei:
+        _abi.check(_abi.lib().taco_allreduce_sim_dev(C.byref(cfg), None, 0, 1, 16, None, 0, None, None, None,
+                                                     None))
+    assert ei.value.code == "usage"
+
+
+def test_flag_mapping():
+    with pytest.raises(TacoError, match="input tensor contains NaN or Inf"):
+        _abi.check(_abi.lib().taco_flags_status(_abi.FLAG_NONFINITE_INPUT))
+    with pytest.raises(TacoError, match="block scalars must be finite and nonzero"):
+        _abi.check(_abi.lib().taco_flags_status(_abi.FLAG_BAD_SCALARS))
+    _abi.check(_abi.lib().taco_flags_status(0))
+
+
+@pytest.mark.parametrize("b", [2, 4, 8, 16, 32, 64, 128, 256, 512, 1024, 4096, 32768])
+@pytest.mark.parametrize("m", [1, 3, 40960])
+def test_message_layout(b, m):
+    lay = _abi.msg_layout(make_config(b), m)
+    assert lay.codes_bytes == m * b
+    assert lay.scal_offset % 16 == 0 and lay.scal_offset >= m * b
+    assert lay.msg_bytes == lay.scal_offset + 8 * m
+    assert lay.msg_stride % 16 == 0 and lay.msg_stride >= lay.msg_bytes
+    if b >= 16:
+        assert lay.msg_bytes == m * (b + 8)  # the reference's per-block wire cost
+
+
+def test_byte_accounting_matches_reference(ref):
+    for b in (32, 256, 512):
+        cfg = make_config(b)
+        for n in (1, 1000, 1_000_000, 10_485_760):
+            assert _abi.lib().taco_archive_size(C.byref(cfg), n) == ref.archive_size(n, b)
+            assert _abi.lib().taco_compressed_ratio(C.byref(cfg), n) == ref.compressed_ratio(n, b)
+    assert _abi.lib().taco_archive_size(C.byref(make_config()), 1_000_000) == 1_031_470
+
+
+def test_product_does_not_reference_the_oracle():
+    import pathlib
+    pkg = pathlib.Path(_abi.PKG_DIR)
+    for f in list(pkg.rglob("*.py")) + list(pkg.rglob("*.cu")) + list(pkg.rglob("*.cpp")):
+        text = f.read_text()
+        assert "oracle" not in text.replace("oracle/", "").lower() or f.name == "__init__.py", f
+    out = subprocess.run(["nm", "-D", _abi.LIB_PATH], capture_output=True, text=True).stdout
+    names = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    assert not any(s.startswith(("tor_", "ref_")) for s in names)
