@@ -8,18 +8,17 @@ using namespace taco_dev;
 namespace {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
-    const uint64_t jobs = (uint64_t)a.P * a.nblk;
-    if (jobs == 0) return cudaSuccess;
+    if (a.nblk == 0 || a.P == 0) return cudaSuccess;
     if constexpr (B <= 1024) {
-        constexpr int VMAX = 16 / (int)sizeof(T);
-        using Gm = Geo<B, 32, VMAX>;
-        k_compress<B, T, FMT, 32, VMAX><<<warp_grid(jobs, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
+        constexpr int VMAX = 8, EMAX = FMT == 0 ? 64 : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
+        using Gm = Geo<B, EMAX, VMAX>;
+        k_compress<B, T, FMT, EMAX, VMAX><<<dim3(warp_grid(a.nblk, Gm::G, kWarpThreads), a.P), kWarpThreads, 0, l.stream>>>(
             static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c);
     } else {
-        const size_t smem = (size_t)B * sizeof(float);
+        const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_compress_big<B, T, FMT>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        kern<<<(unsigned)jobs, kBigThreads, smem, l.stream>>>(static_cast<const T*>(l.in),
+        kern<<<dim3((unsigned)a.nblk, a.P), kBigThreads, smem, l.stream>>>(static_cast<const T*>(l.in),
                                                               static_cast<uint8_t*>(l.out), a, c);
     }
     return cudaGetLastError();

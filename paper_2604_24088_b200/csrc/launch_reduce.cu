@@ -14,7 +14,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         k_reduce_encode<B, T, FMT, 32, 8><<<warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
             static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
     } else {
-        const size_t smem = (size_t)B * sizeof(float);
+        const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_reduce_encode_big<B, T, FMT>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<(unsigned)a.nblk, kBigThreads, smem, l.stream>>>(static_cast<const uint8_t*>(l.in),

@@ -508,18 +508,16 @@ template <int FMT>
 __global__ void k_fp8_encode(const float* __restrict__ x, uint64_t n, uint8_t* __restrict__ out) {
     const uint64_t i = 2 * ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x);
     if (i + 1 < n) {
-        *reinterpret_cast<uint16_t*>(out + i) = (uint16_t)taco_dev::enc2<FMT>(x[i], x[i + 1]);
+        *reinterpret_cast<uint16_t*>(out + i) = (uint16_t)taco_dev::enc2<FMT>(make_float2(x[i], x[i + 1]));
     } else if (i < n) {
-        out[i] = (uint8_t)taco_dev::enc2<FMT>(x[i], 0.0f);
+        out[i] = (uint8_t)taco_dev::enc2<FMT>(make_float2(x[i], 0.0f));
     }
 }
 template <int FMT>
 __global__ void k_fp8_decode(const uint8_t* __restrict__ c, uint64_t n, float* __restrict__ out) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) {
-        float lo, hi;
-        taco_dev::dec2<FMT>(c[i], lo, hi);
-        out[i] = lo;
+        out[i] = taco_dev::dec2<FMT>(c[i]).x;
     }
 }
 }  // namespace

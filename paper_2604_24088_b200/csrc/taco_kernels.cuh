@@ -4,9 +4,10 @@
 //   K2 k_decompress      message(s)            -> y (bf16|f32), valid prefix only
 //   K3 k_reduce_encode   P messages of a shard -> fp32 ascending-rank sum -> message
 //
-// Warp kernels (B <= 1024) keep a whole block in registers of an L-lane group
+// Warp kernels (B <= 32*EMAX) keep whole blocks in registers of L-lane groups
 // (taco_device.cuh); big-block kernels (B >= 2048) stage one block per CTA in shared
 // memory.  All of them read their input once and write their output once.
+// Grid: blockIdx.y = shard (K1/K2), blockIdx.x * warps * G + g = block of the chunk.
 #pragma once
 
 #include "taco_device.cuh"
@@ -28,6 +29,10 @@ struct ShardArgs {
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
 constexpr int kBigThreads = 512;   // one block per CTA for B >= 2048
 
+// E4M3 rotates in packed fp32, E5M2 in fp64 (see RegsD)
+template <int FMT, int E>
+using RegsFor = typename std::conditional<FMT == 0, RegsF<E>, RegsD<E>>::type;
+
 __device__ __forceinline__ void raise_flag(int* flags, int bit) {
     if (flags) atomicOr(flags, bit);
 }
@@ -39,47 +44,20 @@ __device__ __forceinline__ int clamp_valid(int64_t a, int64_t b, int B) {
 }
 
 // Rotate + quantise a register-resident block (rotate_block codec.cpp:45-62 and
-// compress_block_taco :64-76).  On return v holds Z/s, ready for the FP8 cvt.
-template <int V, int L, int E>
-__device__ __forceinline__ void quantise_regs(float (&v)[E], int q, const CodecConsts& c, float& alpha,
-                                              float& s, double& sumsq) {
-    double ss = 0.0;
-#pragma unroll
-    for (int i = 0; i < E; ++i) ss = fma((double)v[i], (double)v[i], ss);  // x^2 exact in double
-    ss = group_sum<L>(ss);
-    sumsq = ss;
+// compress_block_taco :64-76).  On return the values hold Z/s, ready for the cvt.
+template <int L, typename R>
+__device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, float& alpha, float& s, double& ss) {
+    ss = group_sum<L>(v.sumsq());
     alpha = block_alpha(ss, c);
     const float p2 = pow2_near(alpha);
+    v.mul(p2);  // exact power-of-two pre-scale
+    v.template hadamard<L>(q);
+    double ymax = v.absmax();
 #pragma unroll
-    for (int i = 0; i < E; ++i) v[i] *= p2;
-    fwht<V, L, E>(v, q);
-    float ym = 0.0f;
-#pragma unroll
-    for (int i = 0; i < E; ++i) ym = fmaxf(ym, fabsf(v[i]));
-    ym = group_max<L>(ym);
-    float k;
-    block_scale(ym, alpha, p2, c, s, k);
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] *= k;
-}
-
-// Decode one block of a message into registers: yhat*m (decompress_block :144-155).
-// Every lane of the warp executes the butterfly (dead groups on zeros) so the
-// shuffles stay converged.
-template <int FMT, int V, int L, int E>
-__device__ __forceinline__ void dequantise_regs(float (&v)[E], bool live, const uint8_t* __restrict__ codes,
-                                                float2 sc, int q, const CodecConsts& c) {
-    if (live) {
-#pragma unroll
-        for (int j = 0; j < E / V; ++j) load_codes<FMT, V>(codes + (j * L + q) * V, &v[j * V]);
-    } else {
-#pragma unroll
-        for (int i = 0; i < E; ++i) v[i] = 0.0f;
-    }
-    fwht<V, L, E>(v, q);
-    const float m = live ? block_dequant(sc.x, sc.y, c) : 0.0f;
-#pragma unroll
-    for (int i = 0; i < E; ++i) v[i] *= m;
+    for (int m = 1; m < L; m <<= 1) ymax = fmax(ymax, __shfl_xor_sync(kFull, ymax, m));
+    double k;
+    block_scale(ymax, alpha, p2, c, s, k);
+    v.mul(k);
 }
 
 // --------------------------------------------------------------------------- K1 ---
@@ -89,37 +67,38 @@ __global__ void __launch_bounds__(kWarpThreads) k_compress(const TIn* __restrict
     using Gm = Geo<B, EMAX, VMAX>;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L;
-    const uint64_t warp = (uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
-    const uint64_t job = warp * G + g;
-    const bool live = job < (uint64_t)a.P * a.nblk;
-    const uint64_t p = live ? job / a.nblk : 0;
-    const uint64_t kk = live ? job - p * a.nblk : 0;
+    const uint64_t p = blockIdx.y;
+    const uint64_t kk = ((uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5)) * G + g;
+    const bool live = kk < a.nblk;
     const uint64_t k = a.blk0 + kk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B),
                                          (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
                            : 0;
     const TIn* src = x + (p * a.S + k * B);
 
-    float v[E];
+    RegsFor<FMT, E> v;
+    if (__all_sync(kFull, a.vec_ok && valid == B)) {  // warp-uniform fast path
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-        const int pos = Gm::pos(j, q);
-        if (a.vec_ok && pos + V <= valid) {
-            load_vec<TIn, V>(src + pos, &v[j * V]);
-        } else {
+        for (int j = 0; j < NV; ++j) v.template load<TIn, V>(j, src + Gm::pos(j, q));
+    } else {
 #pragma unroll
-            for (int r = 0; r < V; ++r) v[j * V + r] = pos + r < valid ? to_f32(src[pos + r]) : 0.0f;
+        for (int j = 0; j < NV; ++j) {
+            const int pos = Gm::pos(j, q);
+            if (a.vec_ok && pos + V <= valid) v.template load<TIn, V>(j, src + pos);
+            else v.template load_guarded<TIn, V>(j, src + pos, pos, valid);
         }
     }
     float alpha, s;
     double ss;
-    quantise_regs<V, L, E>(v, q, c, alpha, s, ss);
+    quantise<L>(v, q, c, alpha, s, ss);
     if (!live) return;
-    if (q == 0 && !isfinite(ss)) raise_flag(a.flags, 1);
     uint8_t* m = msgs + p * a.msg_stride;
 #pragma unroll
-    for (int j = 0; j < NV; ++j) store_codes<FMT, V>(m + kk * B + Gm::pos(j, q), &v[j * V]);
-    if (q == 0) *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
+    for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
+    if (q == 0) {
+        *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
+        if (!isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
+    }
 }
 
 // --------------------------------------------------------------------------- K2 ---
@@ -129,31 +108,37 @@ __global__ void __launch_bounds__(kWarpThreads) k_decompress(const uint8_t* __re
     using Gm = Geo<B, EMAX, VMAX>;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L;
-    const uint64_t warp = (uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
-    const uint64_t job = warp * G + g;
-    const bool live = job < (uint64_t)a.P * a.nblk;
-    const uint64_t p = live ? job / a.nblk : 0;
-    const uint64_t kk = live ? job - p * a.nblk : 0;
+    const uint64_t p = blockIdx.y;
+    const uint64_t kk = ((uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5)) * G + g;
+    const bool live = kk < a.nblk;
     const uint64_t k = a.blk0 + kk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B),
                                          (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
                            : 0;
     const uint8_t* m = msgs + p * a.msg_stride;
-    float v[E];
-    const float2 sc = live ? __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8)) : make_float2(1.0f, 1.0f);
-    dequantise_regs<FMT, V, L, E>(v, live, m + kk * B, sc, q, c);
+    RegsFor<FMT, E> v;
+    float2 sc = make_float2(1.0f, 1.0f);
+    if (live) {
+        sc = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8));
+#pragma unroll
+        for (int j = 0; j < NV; ++j) v.template load_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
+    } else {
+        v.zero();
+    }
+    v.template hadamard<L>(q);  // every lane takes part: the shuffles stay converged
+    v.mul(block_dequant(sc.x, sc.y, c));
     if (!live) return;
     if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
     TOut* dst = out + (p * a.S + k * B);
+    if (a.vec_ok && valid == B) {
 #pragma unroll
-    for (int j = 0; j < NV; ++j) {
-        const int pos = Gm::pos(j, q);
-        if (a.vec_ok && pos + V <= valid) {
-            store_vec<TOut, V>(dst + pos, &v[j * V]);
-        } else {
+        for (int j = 0; j < NV; ++j) v.template store<TOut, V>(j, dst + Gm::pos(j, q));
+    } else {
 #pragma unroll
-            for (int r = 0; r < V; ++r)
-                if (pos + r < valid) store_one(dst + pos + r, v[j * V + r]);
+        for (int j = 0; j < NV; ++j) {
+            const int pos = Gm::pos(j, q);
+            if (a.vec_ok && pos + V <= valid) v.template store<TOut, V>(j, dst + pos);
+            else v.template store_guarded<TOut, V>(j, dst + pos, pos, valid);
         }
     }
 }
@@ -168,75 +153,75 @@ __global__ void __launch_bounds__(kWarpThreads) k_reduce_encode(const uint8_t* _
     using Gm = Geo<B, EMAX, VMAX>;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L;
-    const uint64_t warp = (uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5);
-    const uint64_t kk = warp * G + g;
+    const uint64_t kk = ((uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5)) * G + g;
     const bool live = kk < a.nblk;
     const uint64_t k = a.blk0 + kk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)B, B) : 0;
 
-    float acc[E];
-#pragma unroll
-    for (int i = 0; i < E; ++i) acc[i] = 0.0f;
+    RegsFor<FMT, E> acc;
     bool bad = false;
     for (uint32_t r = 0; r < a.P; ++r) {
         const uint8_t* m = msgs + r * a.msg_stride;
-        float d[E];
-        const float2 sc = live ? __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8)) : make_float2(1.0f, 1.0f);
-        bad |= !scalars_ok(sc.x, sc.y);
-        dequantise_regs<FMT, V, L, E>(d, live, m + kk * B, sc, q, c);
-        if (r == 0) {
+        RegsFor<FMT, E> d;
+        float2 sc = make_float2(1.0f, 1.0f);
+        if (live) {
+            sc = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8));
 #pragma unroll
-            for (int i = 0; i < E; ++i) acc[i] = d[i];  // acc = dec(rank 0), keeps -0.0
+            for (int j = 0; j < NV; ++j) d.template load_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
         } else {
-#pragma unroll
-            for (int i = 0; i < E; ++i) acc[i] += d[i];
+            d.zero();
         }
+        bad |= !scalars_ok(sc.x, sc.y);
+        d.template hadamard<L>(q);
+        d.mul(block_dequant(sc.x, sc.y, c));
+        d.round_to_f32();  // the decoded slice is an fp32 tensor in the reference
+        if (r == 0) acc = d;  // acc = dec(rank 0): keeps -0.0 like the reference
+        else acc.add(d);      // fp32, ascending rank (collective.cpp:95-100)
     }
     // positions past the shard end are padding of the re-encoded slice (collective.cpp:101)
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int pos = Gm::pos(j, q);
-#pragma unroll
-        for (int r = 0; r < V; ++r)
-            if (pos + r >= valid) acc[j * V + r] = 0.0f;
+        if (pos + V > valid) acc.zero_from(j, V, pos, valid);
     }
     if (live && acc_out) {
         TAcc* dst = acc_out + k * B;
 #pragma unroll
         for (int j = 0; j < NV; ++j) {
             const int pos = Gm::pos(j, q);
-            if (a.vec_ok && pos + V <= valid) {
-                store_vec<TAcc, V>(dst + pos, &acc[j * V]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < V; ++r)
-                    if (pos + r < valid) store_one(dst + pos + r, acc[j * V + r]);
-            }
+            if (a.vec_ok && pos + V <= valid) acc.template store<TAcc, V>(j, dst + pos);
+            else acc.template store_guarded<TAcc, V>(j, dst + pos, pos, valid);
         }
     }
     float alpha, s;
     double ss;
-    quantise_regs<V, L, E>(acc, q, c, alpha, s, ss);
+    quantise<L>(acc, q, c, alpha, s, ss);
     if (!live) return;
-    if (q == 0 && bad) raise_flag(a.flags, 2);
 #pragma unroll
-    for (int j = 0; j < NV; ++j) store_codes<FMT, V>(out_msg + kk * B + Gm::pos(j, q), &acc[j * V]);
-    if (q == 0) *reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8) = make_float2(alpha, s);
+    for (int j = 0; j < NV; ++j) acc.template store_codes_at<FMT, V>(j, out_msg + kk * B + Gm::pos(j, q));
+    if (q == 0) {
+        *reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8) = make_float2(alpha, s);
+        if (bad) raise_flag(a.flags, 2);
+    }
 }
 
 // ===================================================== big blocks (B >= 2048) ===
 // One CTA of kBigThreads per block.  Thread t owns positions t + i*T (i < PER) in
-// registers; butterflies run through shared memory.
+// registers; the butterflies run through shared memory of type W (fp32 for E4M3,
+// fp64 for E5M2 up to B = 16384 -- 128 KB).
 
-template <int B>
-__device__ __forceinline__ void smem_fwht(float* sm) {
+template <int FMT, int B>
+using BigW = typename std::conditional<FMT == 1 && B <= 16384, double, float>::type;
+
+template <int B, typename W>
+__device__ __forceinline__ void smem_fwht(W* sm) {
     constexpr int T = kBigThreads;
 #pragma unroll 1
     for (int h = 1; h < B; h <<= 1) {
         __syncthreads();
         for (int t = threadIdx.x; t < B / 2; t += T) {
             const int i = (t / h) * 2 * h + (t % h);
-            const float a = sm[i], b = sm[i + h];
+            const W a = sm[i], b = sm[i + h];
             sm[i] = a + b;
             sm[i + h] = a - b;
         }
@@ -255,20 +240,20 @@ __device__ __forceinline__ double cta_sum(double v, double* red) {
     return t;
 }
 
-__device__ __forceinline__ float cta_max(float v, float* red) {
+__device__ __forceinline__ double cta_max(double v, double* red) {
 #pragma unroll
-    for (int m = 1; m < 32; m <<= 1) v = fmaxf(v, __shfl_xor_sync(kFull, v, m));
+    for (int m = 1; m < 32; m <<= 1) v = fmax(v, __shfl_xor_sync(kFull, v, m));
     __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
     __syncthreads();
-    float t = 0.0f;
-    for (int w = 0; w < kBigThreads / 32; ++w) t = fmaxf(t, red[w]);
+    double t = 0.0;
+    for (int w = 0; w < kBigThreads / 32; ++w) t = fmax(t, red[w]);
     return t;
 }
 
 // Quantise the register block r[PER] (positions t + i*T); writes codes + scalars.
-template <int B, int FMT>
-__device__ __forceinline__ void big_quantise_store(float (&r)[B / kBigThreads], float* sm, double* red,
+template <int B, int FMT, typename W>
+__device__ __forceinline__ void big_quantise_store(float (&r)[B / kBigThreads], W* sm, double* red,
                                                    const CodecConsts& c, uint8_t* codes, float2* scal,
                                                    int* flags) {
     constexpr int T = kBigThreads, PER = B / T;
@@ -279,33 +264,37 @@ __device__ __forceinline__ void big_quantise_store(float (&r)[B / kBigThreads], 
     const float alpha = block_alpha(ss, c);
     const float p2 = pow2_near(alpha);
 #pragma unroll
-    for (int i = 0; i < PER; ++i) sm[threadIdx.x + i * T] = r[i] * p2;
-    smem_fwht<B>(sm);
-    float ym = 0.0f;
+    for (int i = 0; i < PER; ++i) sm[threadIdx.x + i * T] = (W)(r[i] * p2);
+    smem_fwht<B, W>(sm);
+    double ym = 0.0;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) ym = fmaxf(ym, fabsf(sm[threadIdx.x + i * T]));
-    ym = cta_max(ym, reinterpret_cast<float*>(red));
-    float s, k;
+    for (int i = 0; i < PER; ++i) ym = fmax(ym, fabs((double)sm[threadIdx.x + i * T]));
+    ym = cta_max(ym, red);
+    float s;
+    double k;
     block_scale(ym, alpha, p2, c, s, k);
+    const W kw = (W)k;
     for (int t = threadIdx.x; t < B / 2; t += T)
-        reinterpret_cast<uint16_t*>(codes)[t] = (uint16_t)enc2<FMT>(sm[2 * t] * k, sm[2 * t + 1] * k);
+        reinterpret_cast<uint16_t*>(codes)[t] =
+            (uint16_t)enc2<FMT>(make_float2((float)(sm[2 * t] * kw), (float)(sm[2 * t + 1] * kw)));
     if (threadIdx.x == 0) {
         *scal = make_float2(alpha, s);
         if (!isfinite(ss)) raise_flag(flags, 1);
     }
 }
 
-// decode one block into sm (H(table[c]) * m), returns validity of its scalars
-template <int B, int FMT>
-__device__ __forceinline__ bool big_dequantise(const uint8_t* codes, float2 sc, float* sm, const CodecConsts& c) {
+// decode one block into sm (H(table[c]) * m); returns validity of its scalars
+template <int B, int FMT, typename W>
+__device__ __forceinline__ bool big_dequantise(const uint8_t* codes, float2 sc, W* sm, const CodecConsts& c) {
     __syncthreads();
     for (int t = threadIdx.x; t < B / 2; t += kBigThreads) {
-        const uint32_t two = reinterpret_cast<const uint16_t*>(codes)[t];
-        dec2<FMT>(two, sm[2 * t], sm[2 * t + 1]);
+        const float2 d = dec2<FMT>(reinterpret_cast<const uint16_t*>(codes)[t]);
+        sm[2 * t] = d.x;
+        sm[2 * t + 1] = d.y;
     }
-    smem_fwht<B>(sm);
-    const float m = block_dequant(sc.x, sc.y, c);
-    for (int t = threadIdx.x; t < B; t += kBigThreads) sm[t] *= m;
+    smem_fwht<B, W>(sm);
+    const W m = (W)block_dequant(sc.x, sc.y, c);
+    for (int t = threadIdx.x; t < B; t += kBigThreads) sm[t] = (W)(float)(sm[t] * m);
     __syncthreads();
     return scalars_ok(sc.x, sc.y);
 }
@@ -313,11 +302,12 @@ __device__ __forceinline__ bool big_dequantise(const uint8_t* codes, float2 sc, 
 template <int B, typename TIn, int FMT>
 __global__ void __launch_bounds__(kBigThreads) k_compress_big(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
                                                               ShardArgs a, CodecConsts c) {
-    extern __shared__ float sm[];
+    using W = BigW<FMT, B>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    W* sm = reinterpret_cast<W*>(smraw);
     __shared__ double red[kBigThreads / 32];
     constexpr int T = kBigThreads, PER = B / T;
-    const uint64_t job = blockIdx.x;
-    const uint64_t p = job / a.nblk, kk = job - p * a.nblk, k = a.blk0 + kk;
+    const uint64_t p = blockIdx.y, kk = blockIdx.x, k = a.blk0 + kk;
     const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
     const TIn* src = x + (p * a.S + k * B);
     float r[PER];
@@ -327,23 +317,24 @@ __global__ void __launch_bounds__(kBigThreads) k_compress_big(const TIn* __restr
         r[i] = pos < valid ? to_f32(src[pos]) : 0.0f;
     }
     uint8_t* m = msgs + p * a.msg_stride;
-    big_quantise_store<B, FMT>(r, sm, red, c, m + kk * B, reinterpret_cast<float2*>(m + a.scal_off + kk * 8),
-                               a.flags);
+    big_quantise_store<B, FMT, W>(r, sm, red, c, m + kk * B, reinterpret_cast<float2*>(m + a.scal_off + kk * 8),
+                                  a.flags);
 }
 
 template <int B, typename TOut, int FMT>
-__global__ void __launch_bounds__(kBigThreads) k_decompress_big(const uint8_t* __restrict__ msgs, TOut* __restrict__ out,
-                                                                ShardArgs a, CodecConsts c) {
-    extern __shared__ float sm[];
-    const uint64_t job = blockIdx.x;
-    const uint64_t p = job / a.nblk, kk = job - p * a.nblk, k = a.blk0 + kk;
+__global__ void __launch_bounds__(kBigThreads) k_decompress_big(const uint8_t* __restrict__ msgs,
+                                                                TOut* __restrict__ out, ShardArgs a, CodecConsts c) {
+    using W = BigW<FMT, B>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    W* sm = reinterpret_cast<W*>(smraw);
+    const uint64_t p = blockIdx.y, kk = blockIdx.x, k = a.blk0 + kk;
     const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
     const uint8_t* m = msgs + p * a.msg_stride;
     const float2 sc = *reinterpret_cast<const float2*>(m + a.scal_off + kk * 8);
-    const bool ok = big_dequantise<B, FMT>(m + kk * B, sc, sm, c);
+    const bool ok = big_dequantise<B, FMT, W>(m + kk * B, sc, sm, c);
     if (threadIdx.x == 0 && !ok) raise_flag(a.flags, 2);
     TOut* dst = out + (p * a.S + k * B);
-    for (int t = threadIdx.x; t < valid; t += kBigThreads) store_one(dst + t, sm[t]);
+    for (int t = threadIdx.x; t < valid; t += kBigThreads) store_one(dst + t, (float)sm[t]);
 }
 
 template <int B, typename TAcc, int FMT>
@@ -351,7 +342,9 @@ __global__ void __launch_bounds__(kBigThreads) k_reduce_encode_big(const uint8_t
                                                                    uint8_t* __restrict__ out_msg,
                                                                    TAcc* __restrict__ acc_out, ShardArgs a,
                                                                    CodecConsts c) {
-    extern __shared__ float sm[];
+    using W = BigW<FMT, B>;
+    extern __shared__ __align__(16) unsigned char smraw[];
+    W* sm = reinterpret_cast<W*>(smraw);
     __shared__ double red[kBigThreads / 32];
     constexpr int T = kBigThreads, PER = B / T;
     const uint64_t kk = blockIdx.x, k = a.blk0 + kk;
@@ -361,10 +354,10 @@ __global__ void __launch_bounds__(kBigThreads) k_reduce_encode_big(const uint8_t
     for (uint32_t r = 0; r < a.P; ++r) {
         const uint8_t* m = msgs + r * a.msg_stride;
         const float2 sc = *reinterpret_cast<const float2*>(m + a.scal_off + kk * 8);
-        ok &= big_dequantise<B, FMT>(m + kk * B, sc, sm, c);
+        ok &= big_dequantise<B, FMT, W>(m + kk * B, sc, sm, c);
 #pragma unroll
         for (int i = 0; i < PER; ++i) {
-            const float d = sm[threadIdx.x + i * T];
+            const float d = (float)sm[threadIdx.x + i * T];
             acc[i] = r == 0 ? d : acc[i] + d;
         }
     }
@@ -375,8 +368,8 @@ __global__ void __launch_bounds__(kBigThreads) k_reduce_encode_big(const uint8_t
         else if (acc_out) store_one(acc_out + k * B + pos, acc[i]);
     }
     __syncthreads();
-    big_quantise_store<B, FMT>(acc, sm, red, c, out_msg + kk * B,
-                               reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8), nullptr);
+    big_quantise_store<B, FMT, W>(acc, sm, red, c, out_msg + kk * B,
+                                  reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8), nullptr);
     if (threadIdx.x == 0 && !ok) raise_flag(a.flags, 2);
 }
 
