@@ -49,14 +49,20 @@ template <int L, typename R>
 __device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, float& alpha, float& s, double& ss) {
     ss = group_sum<L>(v.sumsq());
     alpha = block_alpha(ss, c);
-    const float p2 = pow2_near(alpha);
-    v.mul(p2);  // exact power-of-two pre-scale
+    // Exact power-of-two pre-scale, only where the butterfly could overflow fp32
+    // (|y| <= B*max|x| <= B*sqrt(ss)); elsewhere p2 = 1 and the multiply is skipped.
+    const bool huge = !(ss < 0x1p160);
+    float p2 = 1.0f;
+    if (__any_sync(kFull, huge)) {
+        p2 = huge ? pow2_near(alpha) : 1.0f;
+        v.mul(p2);
+    }
     v.template hadamard<L>(q);
-    double ymax = v.absmax();
+    auto ymax = v.absmax();
 #pragma unroll
     for (int m = 1; m < L; m <<= 1) ymax = fmax(ymax, __shfl_xor_sync(kFull, ymax, m));
     double k;
-    block_scale(ymax, alpha, p2, c, s, k);
+    block_scale((double)ymax, alpha, p2, c, s, k);
     v.mul(k);
 }
 
@@ -273,10 +279,10 @@ __device__ __forceinline__ void big_quantise_store(float (&r)[B / kBigThreads], 
     float s;
     double k;
     block_scale(ym, alpha, p2, c, s, k);
-    const W kw = (W)k;
+    // k in double: s may be subnormal, which puts k outside the fp32 range
     for (int t = threadIdx.x; t < B / 2; t += T)
         reinterpret_cast<uint16_t*>(codes)[t] =
-            (uint16_t)enc2<FMT>(make_float2((float)(sm[2 * t] * kw), (float)(sm[2 * t + 1] * kw)));
+            (uint16_t)enc2<FMT>(make_float2((float)((double)sm[2 * t] * k), (float)((double)sm[2 * t + 1] * k)));
     if (threadIdx.x == 0) {
         *scal = make_float2(alpha, s);
         if (!isfinite(ss)) raise_flag(flags, 1);
@@ -293,8 +299,8 @@ __device__ __forceinline__ bool big_dequantise(const uint8_t* codes, float2 sc, 
         sm[2 * t + 1] = d.y;
     }
     smem_fwht<B, W>(sm);
-    const W m = (W)block_dequant(sc.x, sc.y, c);
-    for (int t = threadIdx.x; t < B; t += kBigThreads) sm[t] = (W)(float)(sm[t] * m);
+    const double m = block_dequant(sc.x, sc.y, c);
+    for (int t = threadIdx.x; t < B; t += kBigThreads) sm[t] = (W)(float)((double)sm[t] * m);
     __syncthreads();
     return scalars_ok(sc.x, sc.y);
 }
