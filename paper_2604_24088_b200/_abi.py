@@ -12,7 +12,7 @@ import os
 import re
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libtaco_b200.so")
+LIB_PATH = os.environ.get("TACO_B200_LIB") or os.path.join(PKG_DIR, "libtaco_b200.so")  # override: A/B builds
 HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "taco_b200.h")
 
 OK, ERR_USAGE, ERR_CONFIG, ERR_INPUT, ERR_IO, ERR_CORRUPT, ERR_CUDA = range(7)

@@ -10,10 +10,12 @@ template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
     if constexpr (B <= 1024) {
-        constexpr int VMAX = 8, EMAX = FMT == 0 ? 64 : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
-        using Gm = Geo<B, EMAX, VMAX>;
-        k_decompress<B, T, FMT, EMAX, VMAX><<<dim3(warp_grid(a.nblk, Gm::G, kWarpThreads), a.P), kWarpThreads, 0, l.stream>>>(
-            static_cast<const uint8_t*>(l.in), static_cast<T*>(l.out), a, c);
+        constexpr int VMAX = 16, EMAX = FMT == 0 ? TACO_K2_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
+        using Cf = K2Cfg<B, T, FMT, EMAX, VMAX>;
+        const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
+        auto* kern = &k_decompress<B, T, FMT, EMAX, VMAX>;
+        const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
+        kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in), static_cast<T*>(l.out), a, c, (uint32_t)tps);
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_decompress_big<B, T, FMT>;

@@ -66,85 +66,226 @@ __device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, floa
     v.mul(k);
 }
 
-// --------------------------------------------------------------------------- K1 ---
-template <int B, typename TIn, int FMT, int EMAX, int VMAX>
-__global__ void __launch_bounds__(kWarpThreads) k_compress(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
-                                                           ShardArgs a, CodecConsts c) {
-    using Gm = Geo<B, EMAX, VMAX>;
-    constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
-    const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L;
-    const uint64_t p = blockIdx.y;
-    const uint64_t kk = ((uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5)) * G + g;
-    const bool live = kk < a.nblk;
-    const uint64_t k = a.blk0 + kk;
-    const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B),
-                                         (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
-                           : 0;
-    const TIn* src = x + (p * a.S + k * B);
+// ------------------------------------------------------------ async-copy pipeline ---
+// Persistent warps walk tiles of G consecutive blocks (one L-lane group per block).
+// For full tiles every lane cp.async-es its own 16-byte chunks of tile t+1 into a
+// private double-buffered smem slot (chunk c of lane l at (c*32 + l)*16: conflict-free
+// LDS.128, and each lane only ever reads what it copied, so no barrier is needed)
+// while it computes tile t.  Ragged tiles (shard tails, unaligned shards) take the
+// guarded direct-load path.
 
-    RegsFor<FMT, E> v;
-    if (__all_sync(kFull, a.vec_ok && valid == B)) {  // warp-uniform fast path
-#pragma unroll
-        for (int j = 0; j < NV; ++j) v.template load<TIn, V>(j, src + Gm::pos(j, q));
+constexpr int kPipeWarps = 4;    // warps per CTA of the persistent kernels
+constexpr int kPipeMinCtas = 5;  // >= 20 resident warps per SM (caps registers at 102)
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+// raw 16 bytes of T -> pairs
+template <typename T>
+__device__ __forceinline__ void unpack16(const uint4 u, float2* out) {
+    if constexpr (sizeof(T) == 2) {
+        out[0] = bf16x2_to_f2(u.x); out[1] = bf16x2_to_f2(u.y);
+        out[2] = bf16x2_to_f2(u.z); out[3] = bf16x2_to_f2(u.w);
     } else {
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int pos = Gm::pos(j, q);
-            if (a.vec_ok && pos + V <= valid) v.template load<TIn, V>(j, src + pos);
-            else v.template load_guarded<TIn, V>(j, src + pos, pos, valid);
-        }
-    }
-    float alpha, s;
-    double ss;
-    quantise<L>(v, q, c, alpha, s, ss);
-    if (!live) return;
-    uint8_t* m = msgs + p * a.msg_stride;
-#pragma unroll
-    for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
-    if (q == 0) {
-        *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
-        if (!isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
+        out[0] = f2(__uint_as_float(u.x), __uint_as_float(u.y));
+        out[1] = f2(__uint_as_float(u.z), __uint_as_float(u.w));
     }
 }
 
+// tile -> (shard, first block) and whether the whole tile is full and vector-aligned
+template <int B, int G>
+__device__ __forceinline__ bool tile_full(const ShardArgs& a, uint64_t p, uint64_t kk0) {
+    if (!a.vec_ok || kk0 + G > a.nblk) return false;
+    const uint64_t end = (a.blk0 + kk0 + G) * B;  // one past the tile, within the shard
+    return end <= a.S && p * a.S + end <= a.n;
+}
+
+template <int B, typename TIn, int FMT, int EMAX, int VMAX>
+struct K1Cfg {
+    using Gm = Geo<B, EMAX, VMAX>;
+    static constexpr int VB = Gm::V * (int)sizeof(TIn);  // bytes per lane-vector
+    static constexpr bool PIPE = VB % 16 == 0;
+    static constexpr int CPV = PIPE ? VB / 16 : 1;         // 16-byte chunks per vector
+    static constexpr int NCH = Gm::NV * CPV;               // chunks per lane per tile
+    static constexpr int STAGE_U4 = NCH * 32;              // uint4 per warp stage
+    static constexpr size_t SMEM = PIPE ? (size_t)kPipeWarps * 2 * STAGE_U4 * 16 : 0;
+};
+
+// --------------------------------------------------------------------------- K1 ---
+template <int B, typename TIn, int FMT, int EMAX, int VMAX>
+__global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
+                                                              ShardArgs a, CodecConsts c, uint32_t tiles_per_shard) {
+    using Cf = K1Cfg<B, TIn, FMT, EMAX, VMAX>;
+    using Gm = typename Cf::Gm;
+    constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV, CPV = Cf::CPV;
+    constexpr int EPC = 16 / (int)sizeof(TIn);  // elements per chunk
+    extern __shared__ uint4 smem_dyn[];
+    const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
+    uint4* stage_base = smem_dyn + (size_t)warp * 2 * Cf::STAGE_U4;
+    const uint32_t ntiles = a.P * tiles_per_shard;
+    const uint32_t stride = gridDim.x * kPipeWarps;
+    uint32_t t = blockIdx.x * kPipeWarps + warp;
+
+    auto issue = [&](uint32_t tt, int stage) {
+        if constexpr (Cf::PIPE) {
+            const uint64_t p = tt / tiles_per_shard, kk0 = (uint64_t)(tt - p * tiles_per_shard) * G;
+            if (tile_full<B, G>(a, p, kk0)) {
+                const TIn* src = x + (p * a.S + (a.blk0 + kk0 + g) * B);
+                uint4* st = stage_base + stage * Cf::STAGE_U4;
+#pragma unroll
+                for (int j = 0; j < NV; ++j)
+#pragma unroll
+                    for (int h = 0; h < CPV; ++h)
+                        cp_async16(st + (j * CPV + h) * 32 + lane, src + Gm::pos(j, q) + h * EPC);
+            }
+        }
+        cp_async_commit();  // possibly empty: keeps the group count uniform
+    };
+
+    if (t < ntiles) issue(t, 0);
+    for (int it = 0; t < ntiles; t += stride, ++it) {
+        if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
+        else cp_async_commit();
+        const uint64_t p = t / tiles_per_shard, kk0 = (uint64_t)(t - p * tiles_per_shard) * G;
+        const uint64_t kk = kk0 + g;
+        const bool live = kk < a.nblk;
+        const uint64_t k = a.blk0 + kk;
+        RegsFor<FMT, E> v;
+        if (Cf::PIPE && tile_full<B, G>(a, p, kk0)) {
+            cp_async_wait_1();  // this lane's chunks of tile t have landed
+            const uint4* st = stage_base + (it & 1) * Cf::STAGE_U4;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                float2 tmp[V / 2];
+#pragma unroll
+                for (int h = 0; h < CPV; ++h) unpack16<TIn>(st[(j * CPV + h) * 32 + lane], &tmp[h * EPC / 2]);
+                v.template load_pairs<V>(j, tmp);
+            }
+        } else {
+            const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B),
+                                                 (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
+                                   : 0;
+            const TIn* src = x + (p * a.S + k * B);
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int pos = Gm::pos(j, q);
+                if (a.vec_ok && pos + V <= valid) v.template load<TIn, V>(j, src + pos);
+                else v.template load_guarded<TIn, V>(j, src + pos, pos, valid);
+            }
+        }
+        float alpha, s;
+        double ss;
+        quantise<L>(v, q, c, alpha, s, ss);
+        if (live) {
+            uint8_t* m = msgs + p * a.msg_stride;
+#pragma unroll
+            for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
+            if (q == 0) {
+                *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
+                if (!isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
+            }
+        }
+    }
+}
+
+template <int B, typename TOut, int FMT, int EMAX, int VMAX>
+struct K2Cfg {
+    using Gm = Geo<B, EMAX, VMAX>;
+    static constexpr bool PIPE = Gm::V % 16 == 0;       // 16 codes per chunk
+    static constexpr int NCH = PIPE ? Gm::NV * (Gm::V / 16) : 1;
+    static constexpr int STAGE_U4 = NCH * 32;
+    static constexpr size_t SMEM = PIPE ? (size_t)kPipeWarps * 2 * STAGE_U4 * 16 : 0;
+};
+
 // --------------------------------------------------------------------------- K2 ---
 template <int B, typename TOut, int FMT, int EMAX, int VMAX>
-__global__ void __launch_bounds__(kWarpThreads) k_decompress(const uint8_t* __restrict__ msgs, TOut* __restrict__ out,
-                                                             ShardArgs a, CodecConsts c) {
-    using Gm = Geo<B, EMAX, VMAX>;
+__global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_decompress(const uint8_t* __restrict__ msgs,
+                                                                TOut* __restrict__ out, ShardArgs a, CodecConsts c,
+                                                                uint32_t tiles_per_shard) {
+    using Cf = K2Cfg<B, TOut, FMT, EMAX, VMAX>;
+    using Gm = typename Cf::Gm;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
-    const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L;
-    const uint64_t p = blockIdx.y;
-    const uint64_t kk = ((uint64_t)blockIdx.x * (kWarpThreads / 32) + (threadIdx.x >> 5)) * G + g;
-    const bool live = kk < a.nblk;
-    const uint64_t k = a.blk0 + kk;
-    const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B),
-                                         (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
-                           : 0;
-    const uint8_t* m = msgs + p * a.msg_stride;
-    RegsFor<FMT, E> v;
-    float2 sc = make_float2(1.0f, 1.0f);
-    if (live) {
-        sc = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8));
+    constexpr int CPV = Cf::PIPE ? V / 16 : 1;
+    extern __shared__ uint4 smem_dyn[];
+    const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
+    uint4* stage_base = smem_dyn + (size_t)warp * 2 * Cf::STAGE_U4;
+    const uint32_t ntiles = a.P * tiles_per_shard;
+    const uint32_t stride = gridDim.x * kPipeWarps;
+    uint32_t t = blockIdx.x * kPipeWarps + warp;
+    float2 sc_next = make_float2(1.0f, 1.0f);
+
+    auto issue = [&](uint32_t tt, int stage) {
+        const uint64_t p = tt / tiles_per_shard, kk0 = (uint64_t)(tt - p * tiles_per_shard) * G;
+        const uint8_t* m = msgs + p * a.msg_stride;
+        if (kk0 + g < a.nblk) sc_next = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + g) * 8));
+        if constexpr (Cf::PIPE) {
+            if (kk0 + G <= a.nblk) {  // codes of a message are always aligned
+                const uint8_t* src = m + (kk0 + g) * B;
+                uint4* st = stage_base + stage * Cf::STAGE_U4;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) v.template load_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
-    } else {
-        v.zero();
-    }
-    v.template hadamard<L>(q);  // every lane takes part: the shuffles stay converged
-    v.mul(block_dequant(sc.x, sc.y, c));
-    if (!live) return;
-    if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
-    TOut* dst = out + (p * a.S + k * B);
-    if (a.vec_ok && valid == B) {
+                for (int j = 0; j < NV; ++j)
 #pragma unroll
-        for (int j = 0; j < NV; ++j) v.template store<TOut, V>(j, dst + Gm::pos(j, q));
-    } else {
+                    for (int h = 0; h < CPV; ++h) cp_async16(st + (j * CPV + h) * 32 + lane, src + Gm::pos(j, q) + h * 16);
+            }
+        }
+        cp_async_commit();
+    };
+
+    if (t < ntiles) issue(t, 0);
+    for (int it = 0; t < ntiles; t += stride, ++it) {
+        const float2 sc = sc_next;
+        if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
+        else cp_async_commit();
+        const uint64_t p = t / tiles_per_shard, kk0 = (uint64_t)(t - p * tiles_per_shard) * G;
+        const uint64_t kk = kk0 + g;
+        const bool live = kk < a.nblk;
+        const uint64_t k = a.blk0 + kk;
+        const uint8_t* m = msgs + p * a.msg_stride;
+        RegsFor<FMT, E> v;
+        if (Cf::PIPE && kk0 + G <= a.nblk) {
+            cp_async_wait_1();
+            const uint4* st = stage_base + (it & 1) * Cf::STAGE_U4;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int pos = Gm::pos(j, q);
-            if (a.vec_ok && pos + V <= valid) v.template store<TOut, V>(j, dst + pos);
-            else v.template store_guarded<TOut, V>(j, dst + pos, pos, valid);
+            for (int j = 0; j < NV; ++j) {
+                float2 tmp[V / 2];
+#pragma unroll
+                for (int h = 0; h < CPV; ++h) {
+                    const uint4 u = st[(j * CPV + h) * 32 + lane];
+                    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        tmp[h * 8 + 2 * i] = dec2<FMT>(w[i]);
+                        tmp[h * 8 + 2 * i + 1] = dec2<FMT>(w[i] >> 16);
+                    }
+                }
+                v.template load_pairs<V>(j, tmp);
+            }
+        } else if (live) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) v.template load_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
+        } else {
+            v.zero();
+        }
+        v.template hadamard<L>(q);  // every lane takes part: the shuffles stay converged
+        v.mul(block_dequant(live ? sc.x : 1.0f, live ? sc.y : 1.0f, c));
+        if (!live) continue;
+        if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
+        const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
+        TOut* dst = out + (p * a.S + k * B);
+        if (a.vec_ok && valid == B) {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) v.template store<TOut, V>(j, dst + Gm::pos(j, q));
+        } else {
+#pragma unroll
+            for (int j = 0; j < NV; ++j) {
+                const int pos = Gm::pos(j, q);
+                if (a.vec_ok && pos + V <= valid) v.template store<TOut, V>(j, dst + pos);
+                else v.template store_guarded<TOut, V>(j, dst + pos, pos, valid);
+            }
         }
     }
 }

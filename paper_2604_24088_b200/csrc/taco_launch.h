@@ -26,6 +26,25 @@ cudaError_t launch_compress(const Launch& l, const taco_dev::ShardArgs& a, const
 cudaError_t launch_decompress(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
 cudaError_t launch_reduce_encode(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
 
+// persistent grid: enough CTAs to fill every SM at the kernel's occupancy, never more
+// than there are tiles (cached per kernel and device)
+template <typename K>
+inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t tiles, int warps_per_cta) {
+    static int cached_dev = -1, cached_ctas = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != cached_dev) {
+        int sms = 0, per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+        cached_ctas = sms * (per_sm > 0 ? per_sm : 1);
+        cached_dev = dev;
+    }
+    const uint64_t need = (tiles + warps_per_cta - 1) / warps_per_cta;
+    return (unsigned)(need < (uint64_t)cached_ctas ? need : (uint64_t)cached_ctas);
+}
+
 // grid for the warp kernels: one L-lane group per block job
 inline unsigned warp_grid(uint64_t jobs, int blocks_per_warp, int threads) {
     const uint64_t warps = (jobs + blocks_per_warp - 1) / blocks_per_warp;
