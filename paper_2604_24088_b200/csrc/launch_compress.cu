@@ -15,7 +15,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = &k_compress<B, T, FMT, EMAX, VMAX>;
         const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
-        kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c, (uint32_t)tps);
+        kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_compress_big<B, T, FMT>;

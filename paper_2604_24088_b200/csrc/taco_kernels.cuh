@@ -74,8 +74,14 @@ __device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, floa
 // while it computes tile t.  Ragged tiles (shard tails, unaligned shards) take the
 // guarded direct-load path.
 
+// n / d for n < 2^31 with a host-computed magic number (Granlund-Montgomery)
+struct FastDiv {
+    uint32_t d, m, s;
+    __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, m) + n) >> s; }
+};
+
 constexpr int kPipeWarps = 4;    // warps per CTA of the persistent kernels
-constexpr int kPipeMinCtas = 5;  // >= 20 resident warps per SM (caps registers at 102)
+constexpr int kPipeMinCtas = 4;  // >= 16 resident warps per SM (caps registers at 128)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
@@ -118,7 +124,7 @@ struct K1Cfg {
 // --------------------------------------------------------------------------- K1 ---
 template <int B, typename TIn, int FMT, int EMAX, int VMAX>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
-                                                              ShardArgs a, CodecConsts c, uint32_t tiles_per_shard) {
+                                                              ShardArgs a, CodecConsts c, FastDiv tps) {
     using Cf = K1Cfg<B, TIn, FMT, EMAX, VMAX>;
     using Gm = typename Cf::Gm;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV, CPV = Cf::CPV;
@@ -126,13 +132,14 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
     extern __shared__ uint4 smem_dyn[];
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
     uint4* stage_base = smem_dyn + (size_t)warp * 2 * Cf::STAGE_U4;
-    const uint32_t ntiles = a.P * tiles_per_shard;
+    const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kPipeWarps;
     uint32_t t = blockIdx.x * kPipeWarps + warp;
 
     auto issue = [&](uint32_t tt, int stage) {
         if constexpr (Cf::PIPE) {
-            const uint64_t p = tt / tiles_per_shard, kk0 = (uint64_t)(tt - p * tiles_per_shard) * G;
+            const uint32_t p = tps.div(tt);
+        const uint64_t kk0 = (uint64_t)(tt - p * tps.d) * G;
             if (tile_full<B, G>(a, p, kk0)) {
                 const TIn* src = x + (p * a.S + (a.blk0 + kk0 + g) * B);
                 uint4* st = stage_base + stage * Cf::STAGE_U4;
@@ -150,7 +157,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
     for (int it = 0; t < ntiles; t += stride, ++it) {
         if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
         else cp_async_commit();
-        const uint64_t p = t / tiles_per_shard, kk0 = (uint64_t)(t - p * tiles_per_shard) * G;
+        const uint32_t p = tps.div(t);
+        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * G;
         const uint64_t kk = kk0 + g;
         const bool live = kk < a.nblk;
         const uint64_t k = a.blk0 + kk;
@@ -205,7 +213,7 @@ struct K2Cfg {
 template <int B, typename TOut, int FMT, int EMAX, int VMAX>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_decompress(const uint8_t* __restrict__ msgs,
                                                                 TOut* __restrict__ out, ShardArgs a, CodecConsts c,
-                                                                uint32_t tiles_per_shard) {
+                                                                FastDiv tps) {
     using Cf = K2Cfg<B, TOut, FMT, EMAX, VMAX>;
     using Gm = typename Cf::Gm;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV;
@@ -213,13 +221,14 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_decompress(co
     extern __shared__ uint4 smem_dyn[];
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
     uint4* stage_base = smem_dyn + (size_t)warp * 2 * Cf::STAGE_U4;
-    const uint32_t ntiles = a.P * tiles_per_shard;
+    const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kPipeWarps;
     uint32_t t = blockIdx.x * kPipeWarps + warp;
     float2 sc_next = make_float2(1.0f, 1.0f);
 
     auto issue = [&](uint32_t tt, int stage) {
-        const uint64_t p = tt / tiles_per_shard, kk0 = (uint64_t)(tt - p * tiles_per_shard) * G;
+        const uint32_t p = tps.div(tt);
+        const uint64_t kk0 = (uint64_t)(tt - p * tps.d) * G;
         const uint8_t* m = msgs + p * a.msg_stride;
         if (kk0 + g < a.nblk) sc_next = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + g) * 8));
         if constexpr (Cf::PIPE) {
@@ -240,7 +249,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_decompress(co
         const float2 sc = sc_next;
         if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
         else cp_async_commit();
-        const uint64_t p = t / tiles_per_shard, kk0 = (uint64_t)(t - p * tiles_per_shard) * G;
+        const uint32_t p = tps.div(t);
+        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * G;
         const uint64_t kk = kk0 + g;
         const bool live = kk < a.nblk;
         const uint64_t k = a.blk0 + kk;

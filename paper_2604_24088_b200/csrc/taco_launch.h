@@ -4,10 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-namespace taco_dev {
-struct ShardArgs;
-struct CodecConsts;
-}  // namespace taco_dev
+#include "taco_kernels.cuh"
 
 namespace taco_impl {
 
@@ -43,6 +40,13 @@ inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t til
     }
     const uint64_t need = (tiles + warps_per_cta - 1) / warps_per_cta;
     return (unsigned)(need < (uint64_t)cached_ctas ? need : (uint64_t)cached_ctas);
+}
+
+inline taco_dev::FastDiv make_fastdiv(uint32_t d) {
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    const uint32_t m = (uint32_t)((((1ull << s) - d) << 32) / d + 1);
+    return taco_dev::FastDiv{d, m, s};
 }
 
 // grid for the warp kernels: one L-lane group per block job

@@ -1,0 +1,65 @@
+"""Kernel-only timing of K1 / K2 (and K3) for A/B builds: TACO_B200_LIB=<so> python tools/kbench.py.
+
+Not the contract benchmark (bench.py is); prints one line per kernel with GB/s of
+algorithmic bytes, CUDA-event timed on the launching stream, rotating 4 buffer sets."""
+import ctypes as C
+import os
+import statistics
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2604_24088_b200 import _abi, codec  # noqa: E402
+
+
+def main():
+    b = int(os.environ.get("B", "256"))
+    n = int(os.environ.get("N", str(8192 * 2560)))
+    dt = torch.bfloat16 if os.environ.get("DT", "bf16") == "bf16" else torch.float32
+    fmt = int(os.environ.get("FMT", "0"))
+    reps = int(os.environ.get("REPS", "100"))
+    cfg = codec.make_config(b, fmt)
+    m = -(-n // b)
+    lay = _abi.msg_layout(cfg, m)
+    R = 4
+    xs = [torch.randn(n, device="cuda").to(dt) for _ in range(R)]
+    msgs = [torch.empty((1, lay.msg_stride), dtype=torch.uint8, device="cuda") for _ in range(R)]
+    ys = [torch.empty(n, dtype=dt, device="cuda") for _ in range(R)]
+    lib = _abi.lib()
+    st = torch.cuda.Stream()
+    sp = C.c_void_p(st.cuda_stream)
+    dcode = _abi.DT_BF16 if dt == torch.bfloat16 else _abi.DT_F32
+    esz = 2 if dt == torch.bfloat16 else 4
+
+    def k1(i):
+        _abi.check(lib.taco_compress_dev(C.byref(cfg), C.c_void_p(xs[i].data_ptr()), dcode, n, 1, 0, m,
+                                         C.c_void_p(msgs[i].data_ptr()), lay.msg_stride, None, sp))
+
+    def k2(i):
+        _abi.check(lib.taco_decompress_dev(C.byref(cfg), C.c_void_p(msgs[i].data_ptr()), lay.msg_stride, 1, n, 0,
+                                           m, C.c_void_p(ys[i].data_ptr()), dcode, None, sp))
+
+    c = 1 + 8 / b
+    with torch.cuda.stream(st):
+        for name, fn, bpe in (("k1_compress", k1, esz + c), ("k2_decompress", k2, c + esz)):
+            for i in range(8):
+                k1(i % R)
+                fn(i % R)
+            st.synchronize()
+            ts = []
+            for i in range(reps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(st)
+                fn(i % R)
+                e1.record(st)
+                ts.append((e0, e1))
+            st.synchronize()
+            ms = statistics.median(a.elapsed_time(b_) for a, b_ in ts)
+            gbs = bpe * n / (ms * 1e-3) / 1e9
+            print(f"{os.path.basename(os.environ.get('TACO_B200_LIB', 'default'))} {name} B={b} n={n} {dt} "
+                  f"{ms * 1e3:.2f} us  {gbs:.0f} GB/s  frac={gbs / 6537.3:.3f}", flush=True)
+
+
+if __name__ == "__main__":
+    main()
