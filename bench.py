@@ -312,6 +312,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--chunks", type=int, default=4, help="N>1: pipelined chunks per shard")
+    ap.add_argument("--collective", action="store_true", help="run the all-reduce leg even at world size 1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -320,7 +321,7 @@ def main():
         if rank == 0:
             print(json.dumps(run_reference(args, max(world, args.gpus))), flush=True)
         return
-    if world > 1:
+    if world > 1 or args.collective:
         from paper_2604_24088_b200.bench_collective import run_collective
         line = run_collective(args, ROWS, COLS, ClockSampler, peaks)
         if rank == 0:

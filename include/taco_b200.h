@@ -121,7 +121,8 @@ int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_s
  * Message r is read from msgs + r*rank_stride.  `shard_len` = S (positions >= S in
  * the last block are re-zeroed before re-encoding).  acc_out (optional, may be NULL)
  * receives the fp32 stage-1 sum for positions < S of the chunk (the SP reduce-scatter
- * output and the stage-isolated parity hook), in acc_dtype. */
+ * output and the stage-isolated parity hook), in acc_dtype.  out_msg may be NULL
+ * (reduce-scatter: no re-encode); at least one of out_msg / acc_out must be given. */
 int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride,
                            uint32_t nranks, uint64_t shard_len, uint64_t blk_begin,
                            uint64_t blk_end, void* out_msg, void* acc_out, int acc_dtype,

@@ -124,7 +124,7 @@ def decompress(msgs: torch.Tensor, n: int, cfg: Config, shards: int = 1, out_dty
 
 
 def reduce_encode(msgs: torch.Tensor, nranks: int, shard_len: int, cfg: Config, rank_stride: int,
-                  out_msg: torch.Tensor, acc_out: torch.Tensor | None = None,
+                  out_msg: torch.Tensor | None, acc_out: torch.Tensor | None = None,
                   blk: tuple[int, int] | None = None, flags: Flags | None = None, stream=None) -> torch.Tensor:
     """K3: ascending-rank fp32 sum of ``nranks`` decoded messages of one shard, re-encoded.
 

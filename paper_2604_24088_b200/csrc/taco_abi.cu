@@ -180,6 +180,7 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     if (acc_out)
         if (int rc = check_dtype(acc_dtype)) return rc;
     if (nranks == 0) return fail(TACO_ERR_USAGE, "reduction needs at least one rank");
+    if (!out_msg && !acc_out) return fail(TACO_ERR_USAGE, "reduce-encode needs out_msg or acc_out");
     if (shard_len == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
     const uint64_t b = cfg->block_size, m = div_up(shard_len, b);
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;

@@ -350,6 +350,10 @@ __global__ void __launch_bounds__(kWarpThreads) k_reduce_encode(const uint8_t* _
             else acc.template store_guarded<TAcc, V>(j, dst + pos, pos, valid);
         }
     }
+    if (out_msg == nullptr) {  // reduce-scatter: the fp32 sum is the product, no re-encode
+        if (live && q == 0 && bad) raise_flag(a.flags, 2);
+        return;
+    }
     float alpha, s;
     double ss;
     quantise<L>(acc, q, c, alpha, s, ss);
@@ -523,6 +527,10 @@ __global__ void __launch_bounds__(kBigThreads) k_reduce_encode_big(const uint8_t
         const int pos = threadIdx.x + i * T;
         if (pos >= valid) acc[i] = 0.0f;
         else if (acc_out) store_one(acc_out + k * B + pos, acc[i]);
+    }
+    if (out_msg == nullptr) {
+        if (threadIdx.x == 0 && !ok) raise_flag(a.flags, 2);
+        return;
     }
     __syncthreads();
     big_quantise_store<B, FMT, W>(acc, sm, red, c, out_msg + kk * B,

@@ -1,0 +1,107 @@
+"""GPU side of the collective: the CUDA codec speaks exactly the message format the
+schedule (validated bit-exactly under gloo with the oracle codec) expects, for shard and
+chunk geometries; and the schedule runs end to end on NCCL (world size 1 on the single
+GPU available here -- multi-rank NCCL runs in bench.py under torchrun)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from host_codec import HostCodec
+from parity import COLLECTIVE_RELMSE_MAX, DECODE_RELMSE_MAX, check_codec_parity, rel_mse
+
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2604_24088_b200 import _abi, codec, collective  # noqa: E402
+from paper_2604_24088_b200._abi import make_config  # noqa: E402
+
+
+@pytest.mark.parametrize("n,shards,b,chunk", [(100_000, 3, 256, (5, 90)), (8192 * 37 + 5, 4, 128, (0, 20)),
+                                              (65536, 2, 512, (3, 64))])
+def test_cuda_codec_speaks_the_host_codec_format(port, n, shards, b, chunk):
+    cfg = make_config(b)
+    x = port.mixture(n, 5, tail_fraction=0.03)
+    S = -(-n // shards)
+    m = -(-S // b)
+    b0, b1 = chunk
+    b1 = min(b1, m)
+    lay = _abi.msg_layout(cfg, b1 - b0)
+    cc, hc = collective.CudaCodec(), HostCodec(port)
+    gd = torch.empty((shards, lay.msg_stride), dtype=torch.uint8, device="cuda")
+    gh = torch.zeros((shards, lay.msg_stride), dtype=torch.uint8)
+    cc.compress(cfg, torch.from_numpy(x).cuda(), shards, b0, b1, gd)
+    hc.compress(cfg, torch.from_numpy(x), shards, b0, b1, gh)
+    torch.cuda.synchronize()
+    cc.check()
+    for p in range(shards):
+        dc, da, ds = (t.cpu().numpy() for t in codec.split_message(gd[p], cfg, b1 - b0))
+        hc_, ha, hs = (t.numpy() for t in codec.split_message(gh[p], cfg, b1 - b0))
+        check_codec_parity(dc, da, ds, hc_, ha, hs, f"shard {p}")
+    # decode the HOST messages with the CUDA K2 and vice versa
+    yd = torch.zeros(n, dtype=torch.float32, device="cuda")
+    yh = torch.zeros(n, dtype=torch.float32)
+    cc.decompress(cfg, gh.cuda(), n, shards, b0, b1, yd, lay.msg_stride)
+    hc.decompress(cfg, gh, n, shards, b0, b1, yh, lay.msg_stride)
+    torch.cuda.synchronize()
+    assert rel_mse(yd.cpu().numpy(), yh.numpy()) <= DECODE_RELMSE_MAX
+    # K3 on the host-made messages of `shards` "ranks" of one shard
+    acc_d = torch.zeros(S, dtype=torch.float32, device="cuda")
+    acc_h = torch.zeros(S, dtype=torch.float32)
+    red_d = torch.zeros(lay.msg_stride, dtype=torch.uint8, device="cuda")
+    red_h = torch.zeros(lay.msg_stride, dtype=torch.uint8)
+    cc.reduce_encode(cfg, gh.cuda(), shards, S, lay.msg_stride, b0, b1, red_d, acc_d)
+    hc.reduce_encode(cfg, gh, shards, S, lay.msg_stride, b0, b1, red_h, acc_h)
+    torch.cuda.synchronize()
+    assert rel_mse(acc_d.cpu().numpy(), acc_h.numpy()) <= 1e-10
+    # the re-encode, stage-isolated: oracle compress of the GPU's own sum
+    lo, hi = b0 * b, min(b1 * b, S)
+    rc, ra, rs = port.compress(acc_d.cpu().numpy()[lo:hi], b)
+    dc, da, ds = (t.cpu().numpy() for t in codec.split_message(red_d, cfg, b1 - b0))
+    check_codec_parity(dc, da, ds, rc, ra, rs, "K3")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def nccl_world1():
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_nccl_schedule_world1(port, nccl_world1):
+    n = 8192 * 2560
+    cfg = make_config(256)
+    x32 = port.mixture(n, 7)
+    x = torch.from_numpy(x32).cuda().to(torch.bfloat16)
+    for chunks in (1, 4):
+        ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=chunks)
+        ar.stage1 = torch.zeros(ar.shard_len, dtype=torch.float32, device="cuda")
+        y = ar(x)
+        torch.cuda.synchronize()
+        ar.codec.check()
+        # P = 1: stage 1 is one round trip, the result a round trip of that
+        msg = codec.compress(x, cfg)
+        rt1 = codec.decompress(msg, n, cfg)
+        rt2 = codec.decompress(codec.compress(rt1, cfg), n, cfg)
+        assert torch.equal(ar.stage1, rt1)
+        assert torch.equal(y, rt2)
+    rs = collective.CompressedReduceScatter(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=3)
+    assert torch.equal(rs(x), rt1)
+    ag = collective.CompressedAllGather(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=2)
+    assert torch.equal(ag(x), rt1)
+    assert rel_mse(rt1.cpu().numpy(), x.float().cpu().numpy()) < 1e-3
+    assert COLLECTIVE_RELMSE_MAX > 0
