@@ -311,7 +311,8 @@ def main():
     ap.add_argument("--block-size", type=int, default=B)
     ap.add_argument("--cpu-seconds", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--chunks", type=int, default=4, help="N>1: pipelined chunks per shard")
+    ap.add_argument("--chunks", type=int, default=2, help="N>1: pipelined chunks per shard")
+    ap.add_argument("--eager", action="store_true", help="N>1: no CUDA-graph capture of the step")
     ap.add_argument("--collective", action="store_true", help="run the all-reduce leg even at world size 1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

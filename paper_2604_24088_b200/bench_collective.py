@@ -50,9 +50,13 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(R)]
     ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=dev)
     stream = torch.cuda.current_stream()
+    graphs = [collective.Graphed(ar, xs[i], outs[i]) for i in range(R)] if not args.eager else None
 
     def step(i):
-        ar(xs[i % R], outs[i % R])
+        if graphs is not None:
+            graphs[i % R]()
+        else:
+            ar(xs[i % R], outs[i % R])
 
     for i in range(args.warmup):
         step(i)
@@ -84,9 +88,14 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     yh = torch.empty(n, dtype=torch.bfloat16).pin_memory()
     xd = torch.empty_like(xs[0])
 
+    g_e2e = collective.Graphed(ar, xd, outs[0]) if not args.eager else None
+
     def e2e_step(i):
         xd.copy_(xh, non_blocking=True)
-        ar(xd, outs[0])
+        if g_e2e is not None:
+            g_e2e()
+        else:
+            ar(xd, outs[0])
         yh.copy_(outs[0], non_blocking=True)
 
     for i in range(3):
@@ -119,6 +128,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
             "config": {"workload": f"configs[1] tensor per rank, TP={world} FP8 two-shot all-reduce",
                        "shape": [rows, cols], "elements_per_rank": n, "block_size": args.block_size,
                        "format": "E4M3", "chunks": args.chunks, "parallelism": f"tp{world}",
+                       "launch": "eager" if args.eager else "cuda_graph",
                        "l2": f"{R} rotating input/output buffers of {2 * n / 1e6:.0f} MB"},
             "nccl_bf16_allreduce": {"ms_per_step": round(nccl_ms, 5),
                                     "algbw_GBps": round(world * 2 * n / (nccl_ms * 1e-3) / 1e9, 1),

@@ -204,3 +204,26 @@ class CompressedAllGather:
             self.codec.decompress(self.cfg, self.gath[c].view(self.P, -1), n, self.P, b0, b1, out,
                                   self.ch.layouts[c].msg_stride)
         return out
+
+
+class Graphed:
+    """CUDA-graph replay of a collective call on static buffers: the ~3*chunks codec
+    launches and 2*chunks NCCL calls of a step are captured once, so a step costs one
+    graph launch instead of a Python round trip per op (latency-bound at small sizes)."""
+
+    def __init__(self, op, x: torch.Tensor, out: torch.Tensor, warmup: int = 2):
+        self.op, self.x, self.out = op, x, out
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):  # NCCL communicators / workspaces exist before capture
+                op(x, out)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            op(x, out)
+
+    def __call__(self):
+        self.graph.replay()
+        return self.out

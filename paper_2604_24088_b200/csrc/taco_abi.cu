@@ -4,8 +4,10 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "taco_b200.h"
@@ -93,6 +95,25 @@ int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
 }
 
 }  // namespace
+
+namespace taco_impl {
+int resident_ctas(const void* kernel, int threads, size_t smem) {
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find({kernel, dev});
+    if (it != cache.end()) return it->second;
+    int sms = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
+    const int ctas = sms * (per_sm > 0 ? per_sm : 1);
+    cache[{kernel, dev}] = ctas;
+    return ctas;
+}
+}  // namespace taco_impl
 
 // =================================================================== metadata ====
 extern "C" {

@@ -24,22 +24,15 @@ cudaError_t launch_decompress(const Launch& l, const taco_dev::ShardArgs& a, con
 cudaError_t launch_reduce_encode(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c);
 
 // persistent grid: enough CTAs to fill every SM at the kernel's occupancy, never more
-// than there are tiles (cached per kernel and device)
+// than there are tiles.  Occupancy (and the >48 KB smem opt-in) is resolved once per
+// (kernel, device) -- kernels of one signature share a function type, so key by address.
+int resident_ctas(const void* kernel, int threads, size_t smem);
+
 template <typename K>
 inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t tiles, int warps_per_cta) {
-    static int cached_dev = -1, cached_ctas = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (dev != cached_dev) {
-        int sms = 0, per_sm = 0;
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-        cached_ctas = sms * (per_sm > 0 ? per_sm : 1);
-        cached_dev = dev;
-    }
+    const uint64_t ctas = (uint64_t)resident_ctas(reinterpret_cast<const void*>(kernel), threads, smem);
     const uint64_t need = (tiles + warps_per_cta - 1) / warps_per_cta;
-    return (unsigned)(need < (uint64_t)cached_ctas ? need : (uint64_t)cached_ctas);
+    return (unsigned)(need < ctas ? need : ctas);
 }
 
 inline taco_dev::FastDiv make_fastdiv(uint32_t d) {

@@ -104,4 +104,12 @@ def test_nccl_schedule_world1(port, nccl_world1):
     ag = collective.CompressedAllGather(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=2)
     assert torch.equal(ag(x), rt1)
     assert rel_mse(rt1.cpu().numpy(), x.float().cpu().numpy()) < 1e-3
+    # CUDA-graph replay of the whole step (kernels + NCCL) reproduces the eager result
+    ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=2)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = collective.Graphed(ar, x, out)
+    out.zero_()
+    g()
+    torch.cuda.synchronize()
+    assert torch.equal(out, rt2)
     assert COLLECTIVE_RELMSE_MAX > 0
