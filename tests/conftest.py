@@ -39,3 +39,16 @@ def golden(name):
 
 def golden_names(prefix=""):
     return sorted(f[:-4] for f in os.listdir(GOLDEN) if f.endswith(".npz") and f.startswith(prefix))
+
+
+def pytest_terminal_summary(terminalreporter):
+    try:
+        from parity import FLIP_RATE_MAX, FLIP_TALLY
+    except Exception:
+        return
+    if FLIP_TALLY["codes"]:
+        rate = FLIP_TALLY["flips"] / FLIP_TALLY["codes"]
+        terminalreporter.write_line(
+            f"TACO parity: {FLIP_TALLY['flips']} one-ulp code flips in {FLIP_TALLY['codes']} stage-isolated codes "
+            f"(rate {rate:.3g}, gate {FLIP_RATE_MAX}), max distance {FLIP_TALLY['max_ulp']} ulp")
+        assert rate <= FLIP_RATE_MAX, "aggregate flip rate above the gate"

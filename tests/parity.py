@@ -10,6 +10,9 @@ import numpy as np
 import torch
 
 FLIP_RATE_MAX = 1e-4
+FLIP_SLACK = 4  # absolute allowance for small samples (a handful of codes near a rounding tie)
+# session-wide tally of stage-isolated code comparisons (reported by conftest at the end)
+FLIP_TALLY = {"codes": 0, "flips": 0, "max_ulp": 0}
 SCALE_RTOL = 1e-6
 DECODE_RELMSE_MAX = 1e-6
 COLLECTIVE_RELMSE_MAX = 1e-5
@@ -52,7 +55,10 @@ def check_codec_parity(codes, alpha, scale, rcodes, ralpha, rscale, what=""):
     err = np.max(np.abs(scale.astype(np.float64) / rscale - 1.0)) if scale.size else 0.0
     assert err <= SCALE_RTOL, f"{what}: scale rel err {err}"
     flips, worst = code_diff(codes, rcodes)
+    FLIP_TALLY["codes"] += int(codes.size)
+    FLIP_TALLY["flips"] += flips
+    FLIP_TALLY["max_ulp"] = max(FLIP_TALLY["max_ulp"], worst)
     assert worst <= 1, f"{what}: a code is {worst} ulps away"
     rate = flips / max(1, codes.size)
-    assert rate <= FLIP_RATE_MAX, f"{what}: flip rate {rate}"
+    assert flips <= FLIP_RATE_MAX * codes.size + FLIP_SLACK, f"{what}: flip rate {rate} ({flips} flips)"
     return rate
