@@ -10,8 +10,11 @@ template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0) return cudaSuccess;
     if constexpr (B <= 1024) {
-        using Gm = Geo<B, 32, 8>;
-        k_reduce_encode<B, T, FMT, 32, 8><<<warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
+        // the decode geometry of K2 (launch_decompress.cu): fp32 butterflies over the same
+        // bits in the same order, so K3's per-rank decode is bit-identical to K2's
+        constexpr int VMAX = 16, EMAX = FMT == 0 ? TACO_K2_EMAX : 32;
+        using Gm = Geo<B, EMAX, VMAX>;
+        k_reduce_encode<B, T, FMT, EMAX, VMAX><<<warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
             static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
