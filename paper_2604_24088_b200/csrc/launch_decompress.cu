@@ -1,6 +1,7 @@
 // K2 dispatch: block size x output dtype x FP8 format.
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
+#include "taco_tile.cuh"
 
 namespace taco_impl {
 using namespace taco_dev;
@@ -9,6 +10,19 @@ namespace {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+        if (kernel_family() != 2) {
+            constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
+            using Cf = tile::K2T<NB, T>;
+            const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
+            auto* kern = &tile::k_decompress_tile<NB, T>;
+            const unsigned grid = persistent_grid(kern, tile::kTileWarps * 32, Cf::SMEM, tps * a.P, tile::kTileWarps);
+            kern<<<grid, tile::kTileWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in),
+                                                                      static_cast<T*>(l.out), a, c,
+                                                                      make_fastdiv((uint32_t)tps));
+            return cudaGetLastError();
+        }
+    }
     if constexpr (B <= 1024) {
         constexpr int VMAX = 16, EMAX = FMT == 0 ? TACO_K2_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
         using Cf = K2Cfg<B, T, FMT, EMAX, VMAX>;

@@ -1,6 +1,7 @@
 // K3 dispatch: block size x stage-1 output dtype x FP8 format.
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
+#include "taco_tile.cuh"
 
 namespace taco_impl {
 using namespace taco_dev;
@@ -9,6 +10,24 @@ namespace {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+        if (kernel_family() != 2) {  // K2's decode is the tile kernel: decode with the same code
+            constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
+            using Cf = tile::K3T<NB>;
+            auto* kern = &tile::k_reduce_encode_tile<NB, T>;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cf::SMEM);
+                attr = true;
+            }
+            const uint64_t tiles = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
+            const unsigned grid = (unsigned)((tiles + tile::kTileWarps - 1) / tile::kTileWarps);
+            kern<<<grid, tile::kTileWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in),
+                                                                      static_cast<uint8_t*>(l.out),
+                                                                      static_cast<T*>(l.acc), a, c);
+            return cudaGetLastError();
+        }
+    }
     if constexpr (B <= 1024) {
         // the decode geometry of K2 (launch_decompress.cu): fp32 butterflies over the same
         // bits in the same order, so K3's per-rank decode is bit-identical to K2's

@@ -3,6 +3,7 @@
 // RankSet simulation and the pipelined host API.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -73,6 +74,7 @@ CodecConsts consts_of(const taco_config* cfg) {
     c.inv_b = 1.0 / (double)cfg->block_size;
     c.norm = 1.0 / std::sqrt((double)cfg->block_size);  // transform.cpp:56
     c.qmax = cfg->format ? 57344.0 : 448.0;             // fp8.cpp:11-12
+    c.inv_qmax = 1.0 / c.qmax;
     return c;
 }
 
@@ -97,6 +99,33 @@ int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
 }  // namespace
 
 namespace taco_impl {
+int kernel_family() {
+    static const int fam = [] {
+        const char* v = std::getenv("TACO_B200_KERNELS");
+        if (v && std::strcmp(v, "reg") == 0) return 2;
+        if (v && std::strcmp(v, "tile") == 0) return 1;
+        if (v && std::strcmp(v, "r2") == 0) return 3;
+        return 0;
+    }();
+    return fam;
+}
+
+uint32_t* claim_counter() {
+    constexpr int kRing = 1024;
+    static std::mutex mu;
+    static std::map<int, uint32_t*> rings;
+    static std::map<int, uint32_t> next;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    uint32_t*& ring = rings[dev];
+    if (!ring) {
+        if (cudaMalloc(&ring, kRing * sizeof(uint32_t)) != cudaSuccess) return ring = nullptr;
+        if (cudaMemset(ring, 0, kRing * sizeof(uint32_t)) != cudaSuccess) return nullptr;
+    }
+    return ring + (next[dev]++ % kRing);
+}
+
 int resident_ctas(const void* kernel, int threads, size_t smem) {
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, int> cache;

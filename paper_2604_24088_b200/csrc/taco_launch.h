@@ -35,6 +35,15 @@ inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t til
     return (unsigned)(need < ctas ? need : ctas);
 }
 
+// Kernel family for E4M3 (TACO_B200_KERNELS, read once): 0 = default (K1 register
+// kernel, K2/K3 tile kernels), 1 = "tile" (K1 tile too), 2 = "reg" (the register kernels
+// everywhere), 3 = "r2" (K1 r2).  Measured in profiles/README.md.
+int kernel_family();
+
+// A zeroed device counter for one launch of a dynamically scheduled kernel (ring of
+// counters per device; each kernel leaves its counter at zero when it finishes).
+uint32_t* claim_counter();
+
 inline taco_dev::FastDiv make_fastdiv(uint32_t d) {
     uint32_t s = 0;
     while ((1ull << s) < d) ++s;

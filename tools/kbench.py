@@ -47,17 +47,17 @@ def main():
                 k1(i % R)
                 fn(i % R)
             st.synchronize()
-            ts = []
+            # one event pair around REPS back-to-back launches: per-launch event stamps
+            # are quantised (~2 us) on this part
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
             for i in range(reps):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(st)
                 fn(i % R)
-                e1.record(st)
-                ts.append((e0, e1))
+            e1.record(st)
             st.synchronize()
-            ms = statistics.median(a.elapsed_time(b_) for a, b_ in ts)
+            ms = e0.elapsed_time(e1) / reps
             gbs = bpe * n / (ms * 1e-3) / 1e9
-            print(f"{os.path.basename(os.environ.get('TACO_B200_LIB', 'default'))} {name} B={b} n={n} {dt} "
+            print(f"{os.environ.get("TACO_B200_KERNELS", "r2")} {name} B={b} n={n} {dt} "
                   f"{ms * 1e3:.2f} us  {gbs:.0f} GB/s  frac={gbs / 6537.3:.3f}", flush=True)
 
 
