@@ -45,6 +45,26 @@ def peaks() -> dict:
         return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def ncu_traffic(kind: str):
+    """dram read + write bytes per launch of the K1 ('compress') / K2 ('decompress') kernel
+    from the newest committed ncu capture (profiles/*_ncu_traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as f:
+            d = json.load(f)
+        for k in d["kernels"]:
+            if ("k_" + kind) in k["kernel"]:
+                return {"bytes": int(k["dram_read_bytes"] + k["dram_write_bytes"]), "kernel": k["kernel"],
+                        "source": os.path.relpath(files[-1], ROOT),
+                        "note": "ncu replays one launch: writes still L2-resident at kernel end are not counted"}
+    except Exception:
+        return None
+    return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
 
@@ -173,6 +193,7 @@ def run_taco_single(args) -> dict:
     k1_gbs = bpe["k1"] * n / (k1_ms * 1e-3) / 1e9
     k2_gbs = bpe["k2"] * n / (k2_ms * 1e-3) / 1e9
     dominant = ("k1", k1_ms, k1_gbs, bpe["k1"]) if k1_ms >= k2_ms else ("k2", k2_ms, k2_gbs, bpe["k2"])
+    traffic = ncu_traffic("compress" if dominant[0] == "k1" else "decompress")
 
     # ---- e2e through the C-ABI host call (pinned host buffers, H2D + D2H inside the timed region)
     hc = codec.HostContext(0)
@@ -212,7 +233,8 @@ def run_taco_single(args) -> dict:
                    "parallelism": "single GPU"},
         "roofline": {"bound": "hbm", "kernel": dominant[0], "achieved": round(dominant[2], 1),
                      "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(dominant[2] / pk["hbm_gbs"], 4),
-                     "traffic": None, "peak_source": pk["source"],
+                     "traffic": traffic["bytes"] if traffic else None,
+                     "traffic_source": traffic, "peak_source": pk["source"],
                      "algorithmic_bytes_per_launch": int(dominant[3] * n)},
         "kernels": {"k1_compress": {"ms": round(k1_ms, 5), "GBps": round(k1_gbs, 1),
                                     "frac": round(k1_gbs / pk["hbm_gbs"], 4)},

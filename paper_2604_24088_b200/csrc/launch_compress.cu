@@ -3,14 +3,75 @@
 #include "taco_launch.h"
 #include "taco_tile.cuh"
 #include "taco_r2.cuh"
+#include "taco_tc.cuh"
+
+#include <cudaTypedefs.h>
+
+#include <mutex>
 
 namespace taco_impl {
 using namespace taco_dev;
 
 namespace {
+
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// K1 on the tensor cores (taco_tc.cuh): bf16 input, E4M3, B = 256, every shard a whole
+// number of blocks and no ragged tail, 16-byte aligned input.  Returns cudaErrorNotSupported
+// when the launch is not eligible (the caller then uses the CUDA-core kernel).
+cudaError_t run_tc(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    using namespace taco_dev::tc;
+    if (a.S % kB != 0 || a.n != (uint64_t)a.P * a.S || (reinterpret_cast<uintptr_t>(l.in) & 15) != 0)
+        return cudaErrorNotSupported;
+    auto encode = tensor_map_encoder();
+    if (!encode) return cudaErrorNotSupported;
+    const uint64_t nrows = a.n / kB;
+    CUtensorMap map;
+    const cuuint64_t dims[2] = {(cuuint64_t)kB, (cuuint64_t)nrows};
+    const cuuint64_t strides[1] = {(cuuint64_t)kB * 2};
+    const cuuint32_t box[2] = {64, (cuuint32_t)kM};
+    const cuuint32_t estr[2] = {1, 1};
+    if (encode(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(l.in), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorNotSupported;
+    static std::once_flag attr;
+    std::call_once(attr, [] {
+        cudaFuncSetAttribute(&k_compress_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem);
+    });
+    const uint64_t tps = (a.nblk + kM - 1) / kM;
+    const uint64_t ntiles = tps * a.P;
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)(ntiles < (uint64_t)sms ? ntiles : (uint64_t)sms);
+    TcArgs ta{a.S / kB, a.blk0, a.nblk, a.msg_stride, a.scal_off, a.P, a.flags};
+    k_compress_tc<<<grid, kThreads, kSmem, l.stream>>>(map, static_cast<const __nv_bfloat16*>(l.in),
+                                                       static_cast<uint8_t*>(l.out), ta, c,
+                                                       make_fastdiv((uint32_t)tps));
+    return cudaGetLastError();
+}
+
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B == 256 && std::is_same<T, __nv_bfloat16>::value) {
+        if (kernel_family() == 5) {
+            const cudaError_t e = run_tc(l, a, c);
+            if (e != cudaErrorNotSupported) return e;
+        }
+    }
     if constexpr (FMT == 0 && B >= 32 && B <= 1024) {
         if (kernel_family() == 3) {
             using Cf = r2::Cfg<B, T>;
@@ -26,7 +87,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         }
     }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
-        if (kernel_family() == 1) {
+        const int fam = kernel_family();
+        if (fam == 1 || (fam == 0 && std::is_same<T, float>::value)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K1T<NB, T>;
             const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;

@@ -105,6 +105,7 @@ int kernel_family() {
         if (v && std::strcmp(v, "reg") == 0) return 2;
         if (v && std::strcmp(v, "tile") == 0) return 1;
         if (v && std::strcmp(v, "r2") == 0) return 3;
+        if (v && std::strcmp(v, "tc") == 0) return 5;
         return 0;
     }();
     return fam;

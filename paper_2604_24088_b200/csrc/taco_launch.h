@@ -35,9 +35,11 @@ inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t til
     return (unsigned)(need < ctas ? need : ctas);
 }
 
-// Kernel family for E4M3 (TACO_B200_KERNELS, read once): 0 = default (K1 register
-// kernel, K2/K3 tile kernels), 1 = "tile" (K1 tile too), 2 = "reg" (the register kernels
-// everywhere), 3 = "r2" (K1 r2).  Measured in profiles/README.md.
+// Kernel family for E4M3 (TACO_B200_KERNELS, read once).  0 = default, the measured best
+// per case (profiles/README.md): K1 register kernel for bf16 input, K1 tile kernel for fp32
+// input (64 <= B <= 512), K2/K3 tile kernels.  5 = "tc": K1 on the tensor cores for bf16,
+// B = 256 (taco_tc.cuh; parity-exact, slower today).  1 = "tile" (K1 tile for bf16 too),
+// 2 = "reg" (the register kernels everywhere), 3 = "r2" (K1 r2).
 int kernel_family();
 
 // A zeroed device counter for one launch of a dynamically scheduled kernel (ring of

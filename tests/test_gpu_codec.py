@@ -5,6 +5,7 @@ Small cases run the oracle on the same inputs; config-size cases (BASELINE confi
 size-independent properties (round-trip error, determinism, chunk / shard decomposition,
 power-of-two invariance)."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -24,6 +25,7 @@ from paper_2604_24088_b200 import _abi, codec  # noqa: E402
 from paper_2604_24088_b200._abi import TacoError, make_config  # noqa: E402
 
 DEV = "cuda"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def gpu_compress(x: np.ndarray, b=256, fmt=0, dtype=torch.float32, **kw):
@@ -200,6 +202,56 @@ def test_bad_scalars_raise_corrupt():
         with pytest.raises(TacoError, match="block scalars must be finite and nonzero") as ei:
             gpu_decompress(message_from(codes, al2, sc2), 1000)
         assert ei.value.code == "corrupt"
+
+
+# ------------------------------------------------------------- tensor-core K1 ---
+def _tc_k1_parity(port):
+    n = 256 * (128 * 7 + 50)
+    x = port.mixture(n, 11).astype(np.float32)
+    x[256 * 5: 256 * 6] = 0.0
+    x[256 * 9: 256 * 10] = np.where(x[256 * 9: 256 * 10] >= 0, 1e37, -1e37)
+    x[256 * 11: 256 * 12] *= np.float32(1e-38)
+    x = to_bf16_f32(x)
+    msg, codes, al, sc = gpu_compress(x, 256, dtype=torch.bfloat16)
+    rc, ra, rs = port.compress(x, 256)
+    check_codec_parity(codes, al, sc, rc, ra, rs, "bf16 B=256 K1")
+    # chunks of blocks and block-aligned shards reproduce the whole-tensor message
+    cfg = make_config(256)
+    xd = torch.from_numpy(x).to(DEV).to(torch.bfloat16)
+    m = n // 256
+    for b0, b1 in ((0, 128), (77, 700), (128 * 3, m)):
+        part = codec.compress(xd, cfg, blk=(b0, b1))
+        pc, pa, ps = (t.cpu().numpy() for t in codec.split_message(part[0], cfg, b1 - b0))
+        assert np.array_equal(pc, codes[b0 * 256: b1 * 256])
+        assert np.array_equal(pa, al[b0:b1]) and np.array_equal(ps, sc[b0:b1])
+    sh = codec.compress(xd, cfg, shards=2)
+    for i in range(2):
+        one = codec.compress(xd[i * n // 2:(i + 1) * n // 2].contiguous(), cfg)
+        lay = _abi.msg_layout(cfg, m // 2)
+        assert torch.equal(sh[i, : lay.msg_bytes], one[0, : lay.msg_bytes])
+    x = np.ones(256 * 256, np.float32)
+    x[1000] = float("nan")
+    with pytest.raises(TacoError, match="input tensor contains NaN or Inf"):
+        gpu_compress(x, 256, dtype=torch.bfloat16)
+
+
+def test_bf16_b256_k1_parity(port):
+    """bf16, B = 256, block-aligned (the config shape): full and partial 128-block tiles,
+    an all-zero block, an fp32-overflowing block, bf16 subnormals -- default kernels."""
+    _tc_k1_parity(port)
+
+
+def test_tensor_core_k1_parity_subprocess():
+    """The same checks with K1 on tcgen05 (TACO_B200_KERNELS=tc is read once per process,
+    so it runs in a child interpreter)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path[:0] = ['tests', '.']; import pytest; "
+            "sys.exit(pytest.main(['-q', '-x', '-p', 'no:cacheprovider', 'tests/test_gpu_codec.py', "
+            "'-k', 'bf16_b256_k1_parity or config_size']))")
+    env = dict(os.environ, TACO_B200_KERNELS="tc")
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
 
 
 # ------------------------------------------------------------ config-size properties ---
