@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TACO_B200_ABI_VERSION 1
+#define TACO_B200_ABI_VERSION 2
 
 typedef enum {
     TACO_OK = 0,
@@ -54,19 +54,25 @@ typedef enum { TACO_DT_F32 = 0, TACO_DT_BF16 = 1 } taco_dtype;
 #define TACO_FLAG_NONFINITE_INPUT 1 /* -> Input,   "input tensor contains NaN or Inf"         */
 #define TACO_FLAG_BAD_SCALARS 2     /* -> Corrupt, "block scalars must be finite and nonzero" */
 
-/* taco::CodecConfig (codec.hpp:24-33).  kind: 0 = Taco (the only device kind);
- * format: 0 = E4M3, 1 = E5M2 (fp8.hpp:8). */
+/* taco::CodecConfig (codec.hpp:24-33).
+ * kind (codec.hpp:11-17): 0 = Taco (the fused sm_100a hot path), 1 = DirectFp8,
+ *   2 = Int8Uniform, 3 = Identity (payload = 4B raw bytes per block), 4 = AshInt8;
+ * format: 0 = E4M3, 1 = E5M2 (fp8.hpp:8);
+ * direct_scale (codec.hpp:22, DirectFp8 only): 0 = GlobalMax, 1 = Unit, 2 = PerBlockMax.
+ * GlobalMax and Int8Uniform derive one scale per shard (the reference compresses each
+ * shard slice separately, collective.cpp:82-88). */
 typedef struct {
     uint32_t block_size;
     float target_energy;
     float stability_epsilon;
     uint32_t format;
     uint32_t kind;
+    uint32_t direct_scale;
 } taco_config;
 
 typedef struct {
     uint64_t nblocks;
-    uint64_t codes_bytes; /* nblocks * B */
+    uint64_t codes_bytes; /* nblocks * payload (B, or 4B for Identity) */
     uint64_t scal_offset; /* codes_bytes rounded up to 16 */
     uint64_t msg_bytes;   /* scal_offset + 8 * nblocks */
     uint64_t msg_stride;  /* msg_bytes rounded up to 16 */
@@ -86,7 +92,7 @@ int taco_msg_layout(const taco_config* cfg, uint64_t nblocks, taco_layout* out);
 /* ratio of the reference's wire layout, taco::compressed_ratio (codec.hpp:66) */
 double taco_compressed_ratio(const taco_config* cfg, uint64_t n);
 
-/* taco::archive_size_bytes (serialize.hpp:24): 22 + ceil(n/B)*(B+8) */
+/* taco::archive_size_bytes (serialize.hpp:24): 22 + ceil(n/B)*(payload+8) */
 uint64_t taco_archive_size(const taco_config* cfg, uint64_t n);
 
 /* Map the device flags word to the reference's error (TACO_OK if 0). */
@@ -138,6 +144,24 @@ int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype
                            uint32_t nranks, uint64_t n, void* out, int out_dtype, float* stage1,
                            void* work, int* d_flags, void* stream);
 
+/* taco::scaled_spectrum (codec.hpp:70; codec.cpp:306-326): Z/s of every block slot of
+ * the Taco (q_top = q_max) or AshInt8 (q_top = 127) rotation, ceil(n/B)*B fp32 values. */
+int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
+                             float* out, int* d_flags, void* stream);
+
+/* ------------------------------------------------- TACOCMP1 archive -----
+ * serialize.cpp:109-177: "TACOCMP1", kind u8, format id u8, block size u32, length u64,
+ * then per block [payload][alpha f32][scale f32], little endian.  The device functions
+ * convert between that byte stream and the SoA message of one tensor (n elements). */
+int taco_archive_header(const taco_config* cfg, uint64_t n, uint8_t* out22);
+/* archive_bytes (serialize.hpp:15): msg (device) -> archive (device, taco_archive_size bytes) */
+int taco_archive_export_dev(const taco_config* cfg, const void* msg, uint64_t n, void* archive, void* stream);
+/* archive_parse (serialize.hpp:16) header checks, exact reference messages; fills cfg/n */
+int taco_archive_parse_header(const uint8_t* bytes, uint64_t size, taco_config* cfg_out, uint64_t* n_out);
+/* archive (device) -> msg (device); non-finite scalars set TACO_FLAG_BAD_SCALARS */
+int taco_archive_import_dev(const taco_config* cfg, const void* archive, uint64_t n, void* msg, int* d_flags,
+                            void* stream);
+
 /* ------------------------------------------------------------------ host API -------
  * Synchronous calls on host buffers, the shape of the reference's API (host spans in,
  * host vectors out).  A context owns a stream, device buffers and pinned staging; the
@@ -166,6 +190,10 @@ int taco_roundtrip_host(taco_ctx* ctx, const taco_config* cfg, const void* x_hos
  * stage1_host (optional): P*ceil(n/P) f32 ascending-rank sums before re-encoding. */
 int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* inputs_host,
                             uint32_t nranks, uint64_t n, float* result_host, float* stage1_host);
+
+/* taco::scaled_spectrum (codec.hpp:70) of a host tensor: ceil(n/B)*B fp32 values */
+int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float* x_host, uint64_t n,
+                              float* out_host);
 
 /* ---------------------------------------------------------------- diagnostics ------
  * Element-wise FP8 conversion with exactly the instructions K1/K2/K3 use

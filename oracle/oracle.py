@@ -180,6 +180,15 @@ class Ref:
         lib.ref_archive_size.argtypes = [C.c_uint32, C.c_int, C.c_uint64]
         lib.ref_compressed_ratio.restype = C.c_double
         lib.ref_compressed_ratio.argtypes = [C.c_uint32, C.c_int, C.c_uint64]
+        lib.ref_compress2.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32, C.c_float, C.c_float,
+                                      C.c_int, C.c_int, C.c_int, C.POINTER(C.c_uint8), C.POINTER(C.c_float),
+                                      C.POINTER(C.c_float)]
+        lib.ref_archive2.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32, C.c_int, C.c_int, C.c_int,
+                                     C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_uint64)]
+        lib.ref_archive_decode.argtypes = [C.POINTER(C.c_uint8), C.c_uint64, C.POINTER(C.c_float), C.c_uint64,
+                                           C.POINTER(C.c_uint64)]
+        lib.ref_scaled_spectrum.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32, C.c_int, C.c_int,
+                                            C.POINTER(C.c_float)]
         lib.ref_fp8_encode.restype = C.c_uint8
         lib.ref_fp8_encode.argtypes = [C.c_float, C.c_int]
         self.lib = lib
@@ -243,6 +252,41 @@ class Ref:
         self._check(self.lib.ref_archive(_f32p(x), x.size, block_size, fmt, _u8p(buf), cap,
                                          C.byref(size)))
         return buf[: size.value].tobytes()
+
+    def compress2(self, x, block_size=256, fmt=E4M3, kind=0, scope=0, tau=1.0, eps=1e-12):
+        """compress with the DirectFp8 scope (codec.hpp:22): codes (payload bytes), alpha, scale"""
+        x = _f32(x)
+        m = -(-x.size // block_size)
+        pay = 4 * block_size if kind == 3 else block_size
+        codes = np.zeros(max(m * pay, 1), np.uint8)
+        al = np.zeros(max(m, 1), np.float32)
+        sc = np.zeros(max(m, 1), np.float32)
+        self._check(self.lib.ref_compress2(_f32p(x), x.size, block_size, tau, eps, fmt, kind, scope, _u8p(codes),
+                                           _f32p(al), _f32p(sc)))
+        return codes[: m * pay], al[:m], sc[:m]
+
+    def archive2(self, x, block_size=256, fmt=E4M3, kind=0, scope=0) -> bytes:
+        x = _f32(x)
+        pay = 4 * block_size if kind == 3 else block_size
+        cap = 22 + (-(-x.size // block_size)) * (pay + 8)
+        buf = np.zeros(cap, np.uint8)
+        size = C.c_uint64(0)
+        self._check(self.lib.ref_archive2(_f32p(x), x.size, block_size, fmt, kind, scope, _u8p(buf), cap,
+                                          C.byref(size)))
+        return buf[: size.value].tobytes()
+
+    def archive_decode(self, data: bytes, cap: int):
+        raw = np.frombuffer(data, np.uint8).copy()
+        out = np.zeros(max(cap, 1), np.float32)
+        n = C.c_uint64(0)
+        self._check(self.lib.ref_archive_decode(_u8p(raw), raw.size, _f32p(out), cap, C.byref(n)))
+        return out[: n.value]
+
+    def scaled_spectrum(self, x, block_size=256, fmt=E4M3, kind=0):
+        x = _f32(x)
+        out = np.zeros(-(-x.size // block_size) * block_size, np.float32)
+        self._check(self.lib.ref_scaled_spectrum(_f32p(x), x.size, block_size, fmt, kind, _f32p(out)))
+        return out
 
     def archive_size(self, n, block_size=256, kind=0) -> int:
         return int(self.lib.ref_archive_size(block_size, kind, n))

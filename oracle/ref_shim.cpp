@@ -159,6 +159,52 @@ double ref_compressed_ratio(uint32_t b, int kind, uint64_t n) {
     return taco::compressed_ratio(make_cfg(b, 1.0f, 1e-12f, 0, kind), n);
 }
 
+// compress with every CodecConfig field (DirectFp8 scope included)
+int ref_compress2(const float* x, uint64_t n, uint32_t b, float tau, float eps, int fmt, int kind, int scope,
+                  uint8_t* codes, float* alpha, float* scale) {
+    return guarded([&] {
+        auto cfg = make_cfg(b, tau, eps, fmt, kind);
+        cfg.direct_scale = static_cast<taco::DirectScaleScope>(scope);
+        auto ct = taco::compress(std::span<const float>(x, n), cfg);
+        const size_t pay = ct.blocks.empty() ? 0 : ct.blocks[0].payload.size();
+        for (size_t k = 0; k < ct.blocks.size(); ++k) {
+            std::memcpy(codes + k * pay, ct.blocks[k].payload.data(), pay);
+            alpha[k] = ct.blocks[k].alpha;
+            scale[k] = ct.blocks[k].scale;
+        }
+    });
+}
+
+// archive_bytes(compress(x)) for any kind / scope
+int ref_archive2(const float* x, uint64_t n, uint32_t b, int fmt, int kind, int scope, uint8_t* out, uint64_t cap,
+                 uint64_t* size) {
+    return guarded([&] {
+        auto cfg = make_cfg(b, 1.0f, 1e-12f, fmt, kind);
+        cfg.direct_scale = static_cast<taco::DirectScaleScope>(scope);
+        auto bytes = taco::archive_bytes(taco::compress(std::span<const float>(x, n), cfg));
+        *size = bytes.size();
+        std::memcpy(out, bytes.data(), std::min<uint64_t>(cap, bytes.size()));
+    });
+}
+
+// archive_parse -> decompress (the import path) of a byte stream
+int ref_archive_decode(const uint8_t* bytes, uint64_t size, float* out, uint64_t cap, uint64_t* n) {
+    return guarded([&] {
+        auto ct = taco::archive_parse(std::span<const uint8_t>(bytes, size));
+        auto y = taco::decompress(ct);
+        *n = y.size();
+        std::memcpy(out, y.data(), std::min<uint64_t>(cap, y.size()) * sizeof(float));
+    });
+}
+
+// taco::scaled_spectrum (codec.hpp:70)
+int ref_scaled_spectrum(const float* x, uint64_t n, uint32_t b, int fmt, int kind, float* out) {
+    return guarded([&] {
+        auto y = taco::scaled_spectrum(std::span<const float>(x, n), make_cfg(b, 1.0f, 1e-12f, fmt, kind));
+        std::memcpy(out, y.data(), y.size() * sizeof(float));
+    });
+}
+
 uint8_t ref_fp8_encode(float x, int fmt) {
     return taco::fp8_encode(x, fmt ? taco::Fp8Format::e5m2() : taco::Fp8Format::e4m3());
 }

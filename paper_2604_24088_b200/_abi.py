@@ -18,6 +18,9 @@ HEADER = os.path.join(os.path.dirname(PKG_DIR), "include", "taco_b200.h")
 OK, ERR_USAGE, ERR_CONFIG, ERR_INPUT, ERR_IO, ERR_CORRUPT, ERR_CUDA = range(7)
 DT_F32, DT_BF16 = 0, 1
 E4M3, E5M2 = 0, 1
+# taco::CodecKind (codec.hpp:11-17) and DirectScaleScope (codec.hpp:22)
+TACO, DIRECT_FP8, INT8_UNIFORM, IDENTITY, ASH_INT8 = range(5)
+GLOBAL_MAX, UNIT, PER_BLOCK_MAX = range(3)
 FLAG_NONFINITE_INPUT, FLAG_BAD_SCALARS = 1, 2
 
 # taco::ErrorCode names (proj/include/taco/error.hpp:10-16)
@@ -38,11 +41,13 @@ class Config(C.Structure):
     """taco_config == taco::CodecConfig (proj/include/taco/codec.hpp:24-33)."""
 
     _fields_ = [("block_size", C.c_uint32), ("target_energy", C.c_float),
-                ("stability_epsilon", C.c_float), ("format", C.c_uint32), ("kind", C.c_uint32)]
+                ("stability_epsilon", C.c_float), ("format", C.c_uint32), ("kind", C.c_uint32),
+                ("direct_scale", C.c_uint32)]
 
     def __repr__(self):
         return (f"Config(block_size={self.block_size}, target_energy={self.target_energy}, "
-                f"stability_epsilon={self.stability_epsilon}, format={self.format}, kind={self.kind})")
+                f"stability_epsilon={self.stability_epsilon}, format={self.format}, kind={self.kind}, "
+                f"direct_scale={self.direct_scale})")
 
 
 class Layout(C.Structure):
@@ -50,8 +55,10 @@ class Layout(C.Structure):
                 ("msg_bytes", C.c_uint64), ("msg_stride", C.c_uint64)]
 
 
-def make_config(block_size=256, fmt=E4M3, target_energy=1.0, stability_epsilon=1e-12, kind=0) -> Config:
-    return Config(int(block_size), float(target_energy), float(stability_epsilon), int(fmt), int(kind))
+def make_config(block_size=256, fmt=E4M3, target_energy=1.0, stability_epsilon=1e-12, kind=TACO,
+                direct_scale=GLOBAL_MAX) -> Config:
+    return Config(int(block_size), float(target_energy), float(stability_epsilon), int(fmt), int(kind),
+                  int(direct_scale))
 
 
 _P, _U64, _U32, _I = C.c_void_p, C.c_uint64, C.c_uint32, C.c_int
@@ -77,6 +84,12 @@ _SIGNATURES = {
     "taco_decompress_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P, _I]),
     "taco_roundtrip_host": (C.c_int, [_P, C.POINTER(Config), _P, _I, _U64, _P, _I]),
     "taco_allreduce_sim_host": (C.c_int, [_P, C.POINTER(Config), _P, _U32, _U64, _P, _P]),
+    "taco_scaled_spectrum_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _P, _P]),
+    "taco_archive_header": (C.c_int, [C.POINTER(Config), _U64, _P]),
+    "taco_archive_export_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P]),
+    "taco_archive_parse_header": (C.c_int, [_P, _U64, C.POINTER(Config), C.POINTER(C.c_uint64)]),
+    "taco_archive_import_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P, _P]),
+    "taco_scaled_spectrum_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P]),
     "taco_fp8_encode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
     "taco_fp8_decode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
 }

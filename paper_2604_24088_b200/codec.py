@@ -17,7 +17,8 @@ from dataclasses import dataclass
 import torch
 
 from . import _abi
-from ._abi import DT_BF16, DT_F32, E4M3, E5M2, Config, TacoError, make_config  # noqa: F401
+from ._abi import (ASH_INT8, DIRECT_FP8, DT_BF16, DT_F32, E4M3, E5M2, GLOBAL_MAX, IDENTITY,  # noqa: F401
+                   INT8_UNIFORM, PER_BLOCK_MAX, TACO, UNIT, Config, TacoError, make_config)
 
 _DT = {torch.float32: DT_F32, torch.bfloat16: DT_BF16}
 
@@ -154,8 +155,69 @@ def allreduce_sim(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float32, st
     return out
 
 
+def scaled_spectrum(x: torch.Tensor, cfg: Config, flags: Flags | None = None, stream=None) -> torch.Tensor:
+    """taco::scaled_spectrum (codec.hpp:70): Z/s of every block slot, ceil(n/B)*B fp32 values."""
+    _require_cuda(x)
+    x = x.reshape(-1).contiguous()
+    n = x.numel()
+    out = torch.empty(cdiv(n, cfg.block_size) * cfg.block_size, dtype=torch.float32, device=x.device)
+    _abi.check(_abi.lib().taco_scaled_spectrum_dev(C.byref(cfg), _ptr(x), _dtype_code(x.dtype), n, _ptr(out),
+                                                   flags.ptr() if flags else None, C.c_void_p(_stream(stream))))
+    return out
+
+
+def archive_export(msg: torch.Tensor, n: int, cfg: Config, stream=None) -> torch.Tensor:
+    """taco::archive_bytes (serialize.hpp:15) of one message: a uint8 CUDA tensor of
+    taco_archive_size bytes (TACOCMP1 header + [payload][alpha][scale] per block)."""
+    _require_cuda(msg)
+    size = _abi.lib().taco_archive_size(C.byref(cfg), n)
+    out = torch.empty(size, dtype=torch.uint8, device=msg.device)
+    _abi.check(_abi.lib().taco_archive_export_dev(C.byref(cfg), _ptr(msg), n, _ptr(out),
+                                                  C.c_void_p(_stream(stream))))
+    return out
+
+
+def archive_import(archive: torch.Tensor, flags: Flags | None = None, stream=None):
+    """taco::archive_parse (serialize.hpp:16): (config, n, message) from a TACOCMP1 byte
+    stream held in a uint8 CUDA tensor; every malformed input raises the reference's error."""
+    _require_cuda(archive)
+    size = archive.numel()
+    head = archive[: min(size, 22)].cpu().numpy().tobytes()
+    hb = (C.c_uint8 * 22).from_buffer_copy(head + bytes(22 - len(head)))
+    cfg, n = Config(), C.c_uint64()
+    rc = _abi.lib().taco_archive_parse_header(C.cast(hb, C.c_void_p), size, C.byref(cfg), C.byref(n))
+    if rc != _abi.OK:
+        msg = _abi.lib().taco_last_error().decode()
+        if msg == "unexpected end of archive" and n.value and size > 22:
+            # the reference reads blocks in order: a bad scalar before the cut wins
+            _scan_scalars(archive.cpu().numpy(), cfg, (size - 22) // (_payload(cfg) + 8))
+        raise TacoError(rc, msg)
+    msg = torch.empty(_abi.msg_layout(cfg, cdiv(n.value, cfg.block_size)).msg_stride, dtype=torch.uint8,
+                      device=archive.device)
+    own = flags or Flags(archive.device)
+    _abi.check(_abi.lib().taco_archive_import_dev(C.byref(cfg), _ptr(archive), n.value, _ptr(msg), own.ptr(),
+                                                  C.c_void_p(_stream(stream))))
+    if flags is None and int(own.t.item()) & _abi.FLAG_BAD_SCALARS:
+        raise TacoError(_abi.ERR_CORRUPT, "block scalars must be finite")
+    return cfg, n.value, msg
+
+
+def _payload(cfg: Config) -> int:
+    return 4 * cfg.block_size if cfg.kind == IDENTITY else cfg.block_size
+
+
+def _scan_scalars(raw, cfg: Config, complete: int) -> None:
+    import numpy as np
+    rec = _payload(cfg) + 8
+    for k in range(complete):
+        at = 22 + k * rec + _payload(cfg)
+        ab = np.frombuffer(raw[at: at + 8].tobytes(), np.float32)
+        if not np.all(np.isfinite(ab)):
+            raise TacoError(_abi.ERR_CORRUPT, "block scalars must be finite")
+
+
 def split_message(msg: torch.Tensor, cfg: Config, nblocks: int):
-    """(codes [nblocks*B] uint8, alpha [nblocks] f32, scale [nblocks] f32) views of one message."""
+    """(codes [nblocks*payload] uint8, alpha [nblocks] f32, scale [nblocks] f32) views of one message."""
     lay = _abi.msg_layout(cfg, nblocks)
     codes = msg[: lay.codes_bytes]
     scal = msg[lay.scal_offset: lay.scal_offset + 8 * nblocks].view(torch.float32).view(nblocks, 2)

@@ -57,9 +57,14 @@ int check_config(const taco_config* cfg) {
     if (!(cfg->stability_epsilon > 0.0f) || !std::isfinite(cfg->stability_epsilon))
         return fail(TACO_ERR_CONFIG, "stability epsilon must be positive and finite");
     if (cfg->format > 1) return fail(TACO_ERR_CONFIG, "unknown fp8 format");
-    if (cfg->kind != 0)
-        return fail(TACO_ERR_CONFIG, "only CodecKind::Taco is implemented on the device path");
+    if (cfg->kind > 4) return fail(TACO_ERR_CONFIG, "unknown codec kind");
+    if (cfg->direct_scale > 2) return fail(TACO_ERR_CONFIG, "unknown direct-scale scope");
     return TACO_OK;
+}
+
+// payload bytes per block: B codes, or 4B raw bytes for Identity (codec.hpp:39)
+uint64_t payload_of(const taco_config* cfg) {
+    return cfg->kind == 3 ? 4ull * cfg->block_size : (uint64_t)cfg->block_size;
 }
 
 int check_dtype(int dt) {
@@ -78,10 +83,10 @@ CodecConsts consts_of(const taco_config* cfg) {
     return c;
 }
 
-taco_layout layout_of(uint64_t b, uint64_t nblocks) {
+taco_layout layout_of(uint64_t pb, uint64_t nblocks) {  // pb = payload bytes per block
     taco_layout l;
     l.nblocks = nblocks;
-    l.codes_bytes = nblocks * b;
+    l.codes_bytes = nblocks * pb;
     l.scal_offset = align16(l.codes_bytes);
     l.msg_bytes = l.scal_offset + 8 * nblocks;
     l.msg_stride = align16(l.msg_bytes);
@@ -127,6 +132,24 @@ uint32_t* claim_counter() {
     return ring + (next[dev]++ % kRing);
 }
 
+uint32_t* claim_scratch(uint32_t words) {
+    constexpr uint32_t kWords = 1u << 16;
+    static std::mutex mu;
+    static std::map<int, uint32_t*> rings;
+    static std::map<int, uint32_t> next;
+    if (words == 0 || words > kWords) return nullptr;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    uint32_t*& ring = rings[dev];
+    if (!ring && cudaMalloc(&ring, kWords * sizeof(uint32_t)) != cudaSuccess) return ring = nullptr;
+    uint32_t& at = next[dev];
+    if (at + words > kWords) at = 0;
+    uint32_t* p = ring + at;
+    at += words;
+    return p;
+}
+
 int resident_ctas(const void* kernel, int threads, size_t smem) {
     static std::mutex mu;
     static std::map<std::pair<const void*, int>, int> cache;
@@ -159,6 +182,7 @@ taco_config taco_default_config(void) {
     c.stability_epsilon = 1e-12f;
     c.format = 0;
     c.kind = 0;
+    c.direct_scale = 0;
     return c;
 }
 
@@ -166,18 +190,19 @@ int taco_validate_config(const taco_config* cfg) { return check_config(cfg); }
 
 int taco_msg_layout(const taco_config* cfg, uint64_t nblocks, taco_layout* out) {
     if (int rc = check_config(cfg)) return rc;
-    *out = layout_of(cfg->block_size, nblocks);
+    *out = layout_of(payload_of(cfg), nblocks);
     return TACO_OK;
 }
 
 double taco_compressed_ratio(const taco_config* cfg, uint64_t n) {
     if (n == 0 || !cfg) return 0.0;
+    if (cfg->kind == 3) return 1.0;  // Identity (codec.cpp:300)
     const double blocks = (double)div_up(n, cfg->block_size);
     return 4.0 * (double)n / (blocks * ((double)cfg->block_size + 8.0));  // codec.cpp:298-304
 }
 
 uint64_t taco_archive_size(const taco_config* cfg, uint64_t n) {
-    return 22 + div_up(n, cfg->block_size) * ((uint64_t)cfg->block_size + 8);  // serialize.cpp:172-177
+    return 22 + div_up(n, cfg->block_size) * (payload_of(cfg) + 8);  // serialize.cpp:172-177
 }
 
 int taco_flags_status(int flags) {
@@ -197,11 +222,19 @@ int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t
     if (shards == 0) return fail(TACO_ERR_USAGE, "shard count must be positive");
     const uint64_t b = cfg->block_size, S = div_up(n, shards), m = div_up(S, b);
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
-    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    const taco_layout lay = layout_of(payload_of(cfg), blk_end - blk_begin);
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(x) && (shards == 1 || S % 8 == 0), d_flags};
     Launch l{cfg->block_size, dtype, (int)cfg->format, x, msgs, nullptr, (cudaStream_t)stream};
+    if (cfg->kind != 0) {
+        uint32_t* smax = taco_impl::claim_scratch(shards);
+        if (!smax) return fail(TACO_ERR_CUDA, "scratch allocation failed");
+        if (cudaError_t e = taco_impl::launch_compress_kind(l, a, consts_of(cfg), (int)cfg->kind,
+                                                            (int)cfg->direct_scale, smax))
+            return cuda_fail(e, "compress launch");
+        return TACO_OK;
+    }
     if (cudaError_t e = taco_impl::launch_compress(l, a, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
     return TACO_OK;
 }
@@ -214,11 +247,16 @@ int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_s
     if (shards == 0) return fail(TACO_ERR_USAGE, "shard count must be positive");
     const uint64_t b = cfg->block_size, S = div_up(n, shards), m = div_up(S, b);
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
-    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    const taco_layout lay = layout_of(payload_of(cfg), blk_end - blk_begin);
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(out) && (shards == 1 || S % 8 == 0), d_flags};
     Launch l{cfg->block_size, out_dtype, (int)cfg->format, msgs, out, nullptr, (cudaStream_t)stream};
+    if (cfg->kind != 0) {
+        if (cudaError_t e = taco_impl::launch_decompress_kind(l, a, consts_of(cfg), (int)cfg->kind))
+            return cuda_fail(e, "decompress launch");
+        return TACO_OK;
+    }
     if (cudaError_t e = taco_impl::launch_decompress(l, a, consts_of(cfg)))
         return cuda_fail(e, "K2 decompress launch");
     return TACO_OK;
@@ -233,6 +271,8 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     if (nranks == 0) return fail(TACO_ERR_USAGE, "reduction needs at least one rank");
     if (!out_msg && !acc_out) return fail(TACO_ERR_USAGE, "reduce-encode needs out_msg or acc_out");
     if (shard_len == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (cfg->kind != 0)
+        return fail(TACO_ERR_USAGE, "the fused reduce-encode serves CodecKind::Taco (use decompress + compress)");
     const uint64_t b = cfg->block_size, m = div_up(shard_len, b);
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
     const taco_layout lay = layout_of(b, blk_end - blk_begin);
@@ -248,13 +288,18 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
 uint64_t taco_allreduce_sim_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n) {
     if (!cfg || nranks == 0 || n == 0) return 0;
     const uint64_t S = div_up(n, nranks);
-    const taco_layout lay = layout_of(cfg->block_size, div_up(S, cfg->block_size));
-    // phase-1 messages [rank][shard] + re-encoded shards [shard]
-    return (uint64_t)nranks * nranks * lay.msg_stride + (uint64_t)nranks * lay.msg_stride;
+    const taco_layout lay = layout_of(payload_of(cfg), div_up(S, cfg->block_size));
+    // phase-1 messages [rank][shard] + re-encoded shards [shard] (+ fp32 sum and decode
+    // scratch of one shard for the codec kinds without a fused reduce-encode)
+    uint64_t w = (uint64_t)nranks * nranks * lay.msg_stride + (uint64_t)nranks * lay.msg_stride;
+    if (cfg->kind != 0) w += 2 * align16(S * sizeof(float));
+    return w;
 }
 
 // collective.cpp:75-111 on one device: K1 per rank into its P shard messages, K3 per
-// shard over the P ranks' messages (ascending), K2 of the P re-encoded shards.
+// shard over the P ranks' messages (ascending), K2 of the P re-encoded shards.  Codec
+// kinds other than Taco decode each rank's copy, add in fp32 (ascending rank) and
+// compress the sum with their own codec, like the reference's run_twoshot.
 int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype, uint32_t nranks, uint64_t n,
                            void* out, int out_dtype, float* stage1, void* work, int* d_flags, void* stream) {
     if (nranks < 2) return fail(TACO_ERR_USAGE, "allreduce needs at least 2 ranks");
@@ -262,7 +307,7 @@ int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype
     if (int rc = check_config(cfg)) return rc;
     if (int rc = check_dtype(dtype)) return rc;
     const uint64_t P = nranks, S = div_up(n, P), m = div_up(S, cfg->block_size);
-    const taco_layout lay = layout_of(cfg->block_size, m);
+    const taco_layout lay = layout_of(payload_of(cfg), m);
     uint8_t* sent = static_cast<uint8_t*>(work);
     uint8_t* reduced = sent + P * P * lay.msg_stride;
     const uint8_t* in = static_cast<const uint8_t*>(inputs);
@@ -271,13 +316,128 @@ int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype
                                        sent + r * P * lay.msg_stride, lay.msg_stride, d_flags, stream))
             return rc;
     }
+    float* acc = reinterpret_cast<float*>(reduced + P * lay.msg_stride);
+    float* tmp = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(acc) + align16(S * sizeof(float)));
     for (uint64_t s = 0; s < P; ++s) {
-        if (int rc = taco_reduce_encode_dev(cfg, sent + s * lay.msg_stride, P * lay.msg_stride, nranks, S, 0, m,
-                                            reduced + s * lay.msg_stride, stage1 ? stage1 + s * S : nullptr,
-                                            TACO_DT_F32, d_flags, stream))
+        if (cfg->kind == 0) {
+            if (int rc = taco_reduce_encode_dev(cfg, sent + s * lay.msg_stride, P * lay.msg_stride, nranks, S, 0, m,
+                                                reduced + s * lay.msg_stride, stage1 ? stage1 + s * S : nullptr,
+                                                TACO_DT_F32, d_flags, stream))
+                return rc;
+            continue;
+        }
+        for (uint64_t r = 0; r < P; ++r) {  // acc = dec(rank 0); acc += dec(rank r)
+            if (int rc = taco_decompress_dev(cfg, sent + (r * P + s) * lay.msg_stride, lay.msg_stride, 1, S, 0, m,
+                                             r == 0 ? acc : tmp, TACO_DT_F32, d_flags, stream))
+                return rc;
+            if (r > 0)
+                if (cudaError_t e = taco_impl::launch_add_f32(acc, tmp, S, (cudaStream_t)stream))
+                    return cuda_fail(e, "fp32 sum launch");
+        }
+        if (stage1)
+            if (cudaError_t e = cudaMemcpyAsync(stage1 + s * S, acc, S * sizeof(float), cudaMemcpyDeviceToDevice,
+                                                (cudaStream_t)stream))
+                return cuda_fail(e, "stage-1 copy");
+        if (int rc = taco_compress_dev(cfg, acc, TACO_DT_F32, S, 1, 0, m, reduced + s * lay.msg_stride,
+                                       lay.msg_stride, d_flags, stream))
             return rc;
     }
     return taco_decompress_dev(cfg, reduced, lay.msg_stride, nranks, n, 0, m, out, out_dtype, d_flags, stream);
+}
+
+int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, float* out, int* d_flags,
+                             void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint64_t b = cfg->block_size, m = div_up(n, b);
+    ShardArgs a{n, n, 1, 0, m, 0, 0, 0, d_flags};
+    Launch l{cfg->block_size, dtype, (int)cfg->format, x, out, nullptr, (cudaStream_t)stream};
+    const double qtop = cfg->kind == 4 ? 127.0 : (cfg->format ? 57344.0 : 448.0);  // codec.cpp:311-313
+    if (cudaError_t e = taco_impl::launch_scaled_spectrum(l, a, consts_of(cfg), qtop))
+        return cuda_fail(e, "scaled spectrum launch");
+    return TACO_OK;
+}
+
+// ------------------------------------------------ TACOCMP1 archive (serialize.cpp) ----
+// magic "TACOCMP1", kind u8, format id u8, block size u32 LE, length u64 LE, then per
+// block [payload][alpha f32][scale f32] (serialize.cpp:109-124).
+static uint8_t format_id(const taco_config* cfg) {  // serialize.cpp:79-89
+    if (cfg->kind == 2 || cfg->kind == 4) return 2;
+    if (cfg->kind == 3) return 3;
+    return (uint8_t)cfg->format;
+}
+
+int taco_archive_header(const taco_config* cfg, uint64_t n, uint8_t* out22) {
+    if (int rc = check_config(cfg)) return rc;
+    static const char magic[8] = {'T', 'A', 'C', 'O', 'C', 'M', 'P', '1'};
+    std::memcpy(out22, magic, 8);
+    out22[8] = (uint8_t)cfg->kind;
+    out22[9] = format_id(cfg);
+    const uint32_t b = cfg->block_size;
+    std::memcpy(out22 + 10, &b, 4);  // little-endian host (x86-64 / aarch64)
+    std::memcpy(out22 + 14, &n, 8);
+    return TACO_OK;
+}
+
+int taco_archive_export_dev(const taco_config* cfg, const void* msg, uint64_t n, void* archive, void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (n == 0) return fail(TACO_ERR_CORRUPT, "compressed tensor declares zero elements");
+    const uint64_t m = div_up(n, cfg->block_size);
+    const taco_layout lay = layout_of(payload_of(cfg), m);
+    uint8_t hdr[22];
+    taco_archive_header(cfg, n, hdr);
+    if (cudaError_t e = taco_impl::launch_archive(static_cast<const uint8_t*>(msg), static_cast<uint8_t*>(archive),
+                                                  m, payload_of(cfg), lay.scal_offset, hdr, 0, nullptr,
+                                                  (cudaStream_t)stream))
+        return cuda_fail(e, "archive export launch");
+    return TACO_OK;
+}
+
+int taco_archive_import_dev(const taco_config* cfg, const void* archive, uint64_t n, void* msg, int* d_flags,
+                            void* stream) {
+    if (int rc = check_config(cfg)) return rc;
+    if (n == 0) return fail(TACO_ERR_CORRUPT, "archive declares zero elements");
+    const uint64_t m = div_up(n, cfg->block_size);
+    const taco_layout lay = layout_of(payload_of(cfg), m);
+    if (cudaError_t e = taco_impl::launch_archive(static_cast<const uint8_t*>(archive), static_cast<uint8_t*>(msg),
+                                                  m, payload_of(cfg), lay.scal_offset, nullptr, 1, d_flags,
+                                                  (cudaStream_t)stream))
+        return cuda_fail(e, "archive import launch");
+    return TACO_OK;
+}
+
+// archive_parse (serialize.cpp:126-160) header checks, in the reference's order and with its
+// messages (the Reader's end-of-data message is "unexpected end of archive", :35).  A body
+// shorter than the header declares reports "unexpected end of archive" (the caller scans
+// the complete blocks' scalars first, as the reference's sequential reader would).
+int taco_archive_parse_header(const uint8_t* bytes, uint64_t size, taco_config* cfg_out, uint64_t* n_out) {
+    static const char magic[8] = {'T', 'A', 'C', 'O', 'C', 'M', 'P', '1'};
+    static const char* eof = "unexpected end of archive";
+    if (size < 8) return fail(TACO_ERR_CORRUPT, eof);
+    if (std::memcmp(bytes, magic, 8) != 0) return fail(TACO_ERR_CORRUPT, "bad magic, not a compressed archive");
+    if (size < 9) return fail(TACO_ERR_CORRUPT, eof);
+    if (bytes[8] > 4) return fail(TACO_ERR_CORRUPT, "unknown codec kind in archive");
+    if (size < 10) return fail(TACO_ERR_CORRUPT, eof);
+    if (bytes[9] > 3) return fail(TACO_ERR_CORRUPT, "unknown payload format in archive");
+    if (size < 14) return fail(TACO_ERR_CORRUPT, eof);
+    taco_config c = taco_default_config();
+    c.kind = bytes[8];
+    c.format = bytes[9] == 1 ? 1u : 0u;
+    uint32_t b;
+    uint64_t n;
+    std::memcpy(&b, bytes + 10, 4);
+    if (!pow2(b) || b < 2 || b > 32768) return fail(TACO_ERR_CORRUPT, "archive block size is not a valid power of two");
+    if (size < 22) return fail(TACO_ERR_CORRUPT, eof);
+    std::memcpy(&n, bytes + 14, 8);
+    if (n == 0) return fail(TACO_ERR_CORRUPT, "archive declares zero elements");
+    c.block_size = b;
+    *cfg_out = c;
+    *n_out = n;
+    const uint64_t need = 22 + div_up(n, b) * (payload_of(&c) + 8);
+    if (size < need) return fail(TACO_ERR_CORRUPT, eof);
+    if (size > need) return fail(TACO_ERR_CORRUPT, "trailing bytes after archive payload");
+    return TACO_OK;
 }
 
 }  // extern "C"
@@ -397,13 +557,16 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
                                  : fail(TACO_ERR_INPUT, "input tensor is empty");
     std::lock_guard<std::mutex> lock(ctx->mu);
     TACO_CUDA(cudaSetDevice(ctx->device));
-    const uint64_t b = cfg->block_size, m = div_up(n, b);
+    const uint64_t b = cfg->block_size, m = div_up(n, b), pb = payload_of(cfg);
     const size_t ein = mode == 1 ? 1 : dtype_size(in_dtype);
     const size_t eout = mode == 0 ? 1 : dtype_size(out_dtype);
-    const uint64_t cb = chunk_blocks(b, mode == 1 ? 4 : ein);
-    const taco_layout full = layout_of(b, m);
-    const taco_layout cl = layout_of(b, std::min(cb, m));
-    const size_t in_bytes = mode == 1 ? cl.msg_stride : cb * b * ein;
+    // tensor-wide scales (DirectFp8 GlobalMax, Int8Uniform: codec.cpp:223-229) need the
+    // whole tensor in one launch; everything else pipelines in chunks of whole blocks
+    const bool whole = cfg->kind == 2 || (cfg->kind == 1 && cfg->direct_scale == 0);
+    const uint64_t cb = whole ? m : chunk_blocks(b, mode == 1 ? 4 : ein);
+    const taco_layout full = layout_of(pb, m);
+    const taco_layout cl = layout_of(pb, std::min(cb, m));
+    const size_t in_bytes = mode == 1 ? cl.msg_stride : cb * b * ein;  // (payload-aware via cl)
     const size_t out_bytes = mode == 0 ? cl.msg_stride : cb * b * eout;
     if (int rc = grow_dev(ctx->d_in, ctx->cap_in, in_bytes)) return rc;
     if (int rc = grow_dev(ctx->d_msg, ctx->cap_msg, cl.msg_stride)) return rc;
@@ -437,7 +600,7 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         cudaStream_t st = ctx->st[slot];
         const uint64_t b0 = ci * cb, b1 = std::min(m, b0 + cb), nb = b1 - b0;
         const uint64_t e0 = b0 * b, e1 = std::min<uint64_t>(n, b1 * b), ne = e1 - e0;
-        const taco_layout lay = layout_of(b, nb);
+        const taco_layout lay = layout_of(pb, nb);
         if (int rc = drain(slot)) return rc;  // slot buffers free again
         if (!pin_in) TACO_CUDA(cudaStreamSynchronize(st));
         // ---- H2D
@@ -453,7 +616,7 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         };
         if (mode == 1) {  // chunk of the full message -> chunk message layout
             uint8_t* d = static_cast<uint8_t*>(ctx->d_in[slot]);
-            if (int rc = h2d(d, s8 + b0 * b, nb * b, 0)) return rc;
+            if (int rc = h2d(d, s8 + b0 * pb, nb * pb, 0)) return rc;
             if (int rc = h2d(d + lay.scal_offset, s8 + full.scal_offset + b0 * 8, nb * 8, lay.scal_offset)) return rc;
         } else {
             if (int rc = h2d(ctx->d_in[slot], s8 + e0 * ein, ne * ein, 0)) return rc;
@@ -481,8 +644,8 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         };
         if (mode == 0) {
             const uint8_t* d = static_cast<const uint8_t*>(ctx->d_out[slot]);
-            if (int rc = d2h(d8 + b0 * b, d, nb * b, 0)) return rc;
-            if (int rc = d2h(d8 + full.scal_offset + b0 * 8, d + lay.scal_offset, nb * 8, nb * b)) return rc;
+            if (int rc = d2h(d8 + b0 * pb, d, nb * pb, 0)) return rc;
+            if (int rc = d2h(d8 + full.scal_offset + b0 * 8, d + lay.scal_offset, nb * 8, nb * pb)) return rc;
         } else {
             if (int rc = d2h(d8 + e0 * eout, ctx->d_out[slot], ne * eout, 0)) return rc;
         }
@@ -505,6 +668,38 @@ int taco_decompress_host(taco_ctx* ctx, const taco_config* cfg, const void* msg_
 int taco_roundtrip_host(taco_ctx* ctx, const taco_config* cfg, const void* x_host, int dtype, uint64_t n,
                         void* out_host, int out_dtype) {
     return host_pipeline(ctx, cfg, 2, x_host, dtype, n, out_host, out_dtype);
+}
+
+int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float* x_host, uint64_t n,
+                              float* out_host) {
+    if (!ctx) return fail(TACO_ERR_USAGE, "null taco context");
+    if (int rc = check_config(cfg)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    TACO_CUDA(cudaSetDevice(ctx->device));
+    const uint64_t out_n = div_up(n, cfg->block_size) * cfg->block_size;
+    void *d_in = nullptr, *d_out = nullptr;
+    cudaStream_t st = ctx->st[0];
+    int rc = TACO_OK;
+    cudaError_t e = cudaMalloc(&d_in, n * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&d_out, out_n * 4);
+    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, x_host, n * 4, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) rc = cuda_fail(e, "scaled spectrum staging");
+    if (rc == TACO_OK) rc = taco_scaled_spectrum_dev(cfg, d_in, TACO_DT_F32, n, static_cast<float*>(d_out), ctx->d_flags, st);
+    if (rc == TACO_OK) {
+        e = cudaMemcpyAsync(out_host, d_out, out_n * 4, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = cuda_fail(e, "scaled spectrum readback");
+    }
+    if (rc == TACO_OK) {
+        int flags = 0;
+        e = cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
+        rc = e != cudaSuccess ? cuda_fail(e, "flags readback") : taco_flags_status(flags);
+    }
+    cudaFree(d_in);
+    cudaFree(d_out);
+    return rc;
 }
 
 int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* inputs_host, uint32_t nranks,

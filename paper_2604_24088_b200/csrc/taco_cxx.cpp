@@ -58,14 +58,11 @@ taco_config to_c(const CodecConfig& cfg) {
     c.stability_epsilon = cfg.stability_epsilon;
     c.format = cfg.format == Fp8Variant::E5M2 ? 1u : 0u;
     c.kind = static_cast<uint32_t>(cfg.kind);
+    c.direct_scale = static_cast<uint32_t>(cfg.direct_scale);
     return c;
 }
 
-void require_device_kind(CodecKind k) {
-    if (k != CodecKind::Taco)
-        fail(ErrorCode::Config, std::string("codec kind '") + codec_kind_name(k) +
-                                    "' has no device implementation (only taco)");
-}
+size_t payload_bytes(CodecKind k, size_t b) { return k == CodecKind::Identity ? 4 * b : b; }
 
 constexpr Fp8Format kE4M3{Fp8Variant::E4M3, 4, 3, 7, 448.0f, false};
 constexpr Fp8Format kE5M2{Fp8Variant::E5M2, 5, 2, 15, 57344.0f, true};
@@ -193,9 +190,8 @@ float adaptive_scale(float sigma, float tau) { return tau / sigma; }
 CompressedTensor compress(std::span<const float> x, const CodecConfig& cfg) {
     validate_config(cfg);
     if (x.empty()) fail(ErrorCode::Input, "input tensor is empty");
-    require_device_kind(cfg.kind);
     const taco_config c = to_c(cfg);
-    const uint64_t b = cfg.block_size, m = (x.size() + b - 1) / b;
+    const uint64_t b = cfg.block_size, m = (x.size() + b - 1) / b, pb = payload_bytes(cfg.kind, b);
     taco_layout lay;
     check(taco_msg_layout(&c, m, &lay));
     std::vector<uint8_t> msg(lay.msg_bytes);
@@ -208,7 +204,7 @@ CompressedTensor compress(std::span<const float> x, const CodecConfig& cfg) {
     ct.blocks.resize(m);
     const float* scal = reinterpret_cast<const float*>(msg.data() + lay.scal_offset);
     for (uint64_t k = 0; k < m; ++k) {
-        ct.blocks[k].payload.assign(msg.data() + k * b, msg.data() + (k + 1) * b);
+        ct.blocks[k].payload.assign(msg.data() + k * pb, msg.data() + (k + 1) * pb);
         ct.blocks[k].alpha = scal[2 * k];
         ct.blocks[k].scale = scal[2 * k + 1];
     }
@@ -238,14 +234,13 @@ TensorBuffer decompress(const CompressedTensor& ct, const CodecConfig& cfg) {
         if (!std::isfinite(blk.alpha) || !std::isfinite(blk.scale) || blk.scale == 0.0f || blk.alpha == 0.0f)
             fail(ErrorCode::Corrupt, "block scalars must be finite and nonzero");
     }
-    require_device_kind(ct.kind);
     taco_config c = to_c(cfg);
     taco_layout lay;
     check(taco_msg_layout(&c, m, &lay));
     std::vector<uint8_t> msg(lay.msg_bytes);
     float* scal = reinterpret_cast<float*>(msg.data() + lay.scal_offset);
     for (uint64_t k = 0; k < m; ++k) {
-        std::memcpy(msg.data() + k * b, ct.blocks[k].payload.data(), b);
+        std::memcpy(msg.data() + k * payload, ct.blocks[k].payload.data(), payload);
         scal[2 * k] = ct.blocks[k].alpha;
         scal[2 * k + 1] = ct.blocks[k].scale;
     }
@@ -264,7 +259,11 @@ double compressed_ratio(const CodecConfig& cfg, uint64_t n) {
 TensorBuffer scaled_spectrum(std::span<const float> x, const CodecConfig& cfg) {
     validate_config(cfg);
     if (x.empty()) fail(ErrorCode::Input, "input tensor is empty");
-    fail(ErrorCode::Config, "scaled_spectrum has no device implementation");
+    const taco_config c = to_c(cfg);
+    const uint64_t b = cfg.block_size, m = (x.size() + b - 1) / b;
+    TensorBuffer out(m * b);
+    check(taco_scaled_spectrum_host(context(), &c, x.data(), x.size(), out.data()));
+    return out;
 }
 
 const char* codec_kind_name(CodecKind k) {
@@ -310,7 +309,6 @@ AllReduceOutcome allreduce(const RankSet& rs) {
     if (rs.algorithm != Algorithm::TwoShot)
         fail(ErrorCode::Config, std::string("algorithm '") + algorithm_name(rs.algorithm) +
                                     "' has no device implementation (only twoshot)");
-    require_device_kind(rs.codec.kind);
     const size_t p = rs.inputs.size();
     std::vector<float> flat(p * n);
     for (size_t r = 0; r < p; ++r) std::copy(rs.inputs[r].begin(), rs.inputs[r].end(), flat.begin() + r * n);

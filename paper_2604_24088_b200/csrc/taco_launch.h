@@ -46,6 +46,21 @@ int kernel_family();
 // counters per device; each kernel leaves its counter at zero when it finishes).
 uint32_t* claim_counter();
 
+// P zero-able 32-bit scratch words (per-shard scales of the non-Taco codec kinds).
+uint32_t* claim_scratch(uint32_t words);
+
+// the other codec kinds (launch_kinds.cu) and small helpers (launch_misc.cu)
+cudaError_t launch_compress_kind(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c,
+                                 int kind, int scope, uint32_t* smax);
+cudaError_t launch_decompress_kind(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c,
+                                   int kind);
+cudaError_t launch_scaled_spectrum(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c,
+                                   double qtop);
+cudaError_t launch_add_f32(float* acc, const float* x, uint64_t n, cudaStream_t stream);
+// mode 0: SoA message -> TACOCMP1 archive (header from hdr22); mode 1: archive body -> message
+cudaError_t launch_archive(const uint8_t* src, uint8_t* dst, uint64_t nblocks, uint64_t payload, uint64_t scal_off,
+                           const uint8_t* hdr22, int mode, int* flags, cudaStream_t stream);
+
 inline taco_dev::FastDiv make_fastdiv(uint32_t d) {
     uint32_t s = 0;
     while ((1ull << s) < d) ++s;

@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
     exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
     assert set(syms) <= exported
-    assert lib.taco_abi_version() == 1
+    assert lib.taco_abi_version() == 2
 
 
 def test_default_config_matches_reference_defaults():
