@@ -195,6 +195,21 @@ int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* 
 int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float* x_host, uint64_t n,
                               float* out_host);
 
+/* taco::error_report (analysis.hpp:42; analysis.cpp:97-132) on the device:
+ * synchronous, deterministic.  Histogram edges are hist_lo + (hist_hi-hist_lo)/bins * i
+ * (the last edge exactly hist_hi); counts[bins] receives the bin counts. */
+typedef struct {
+    double mse;
+    double relative_l2;
+    double max_abs_error;
+    double zero_collapse_fraction;
+    double kurtosis;
+    int kurtosis_defined;
+    double hist_lo, hist_hi;
+} taco_error_report;
+int taco_error_report_dev(const void* original, int orig_dtype, const void* reconstructed, int recon_dtype,
+                          uint64_t n, uint32_t bins, taco_error_report* out, uint64_t* counts, void* stream);
+
 /* ---------------------------------------------------------------- diagnostics ------
  * Element-wise FP8 conversion with exactly the instructions K1/K2/K3 use
  * (cvt.rn.satfinite.{e4m3,e5m2}x2.f32 / cvt.f16x2.{e4m3,e5m2}x2), replacing

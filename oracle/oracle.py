@@ -189,6 +189,8 @@ class Ref:
                                            C.POINTER(C.c_uint64)]
         lib.ref_scaled_spectrum.argtypes = [C.POINTER(C.c_float), C.c_uint64, C.c_uint32, C.c_int, C.c_int,
                                             C.POINTER(C.c_float)]
+        lib.ref_error_report.argtypes = [C.POINTER(C.c_float), C.POINTER(C.c_float), C.c_uint64, C.c_uint32,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_uint64)]
         lib.ref_fp8_encode.restype = C.c_uint8
         lib.ref_fp8_encode.argtypes = [C.c_float, C.c_int]
         self.lib = lib
@@ -287,6 +289,19 @@ class Ref:
         out = np.zeros(-(-x.size // block_size) * block_size, np.float32)
         self._check(self.lib.ref_scaled_spectrum(_f32p(x), x.size, block_size, fmt, kind, _f32p(out)))
         return out
+
+    def error_report(self, x, y, bins=64) -> dict:
+        x, y = _f32(x), _f32(y)
+        out = np.zeros(8, np.float64)
+        counts = np.zeros(bins, np.uint64)
+        self._check(self.lib.ref_error_report(_f32p(x), _f32p(y), x.size, bins,
+                                              out.ctypes.data_as(C.POINTER(C.c_double)),
+                                              counts.ctypes.data_as(C.POINTER(C.c_uint64))))
+        keys = ["mse", "relative_l2", "max_abs_error", "zero_collapse_fraction", "kurtosis", "kurtosis_defined",
+                "lo", "hi"]
+        d = dict(zip(keys, out.tolist()))
+        d["counts"] = counts.tolist()
+        return d
 
     def archive_size(self, n, block_size=256, kind=0) -> int:
         return int(self.lib.ref_archive_size(block_size, kind, n))

@@ -205,6 +205,23 @@ int ref_scaled_spectrum(const float* x, uint64_t n, uint32_t b, int fmt, int kin
     });
 }
 
+// taco::error_report (analysis.hpp:42): out8 = mse, rel_l2, max_abs, zero_collapse, kurtosis,
+// defined, first edge, last edge; counts[bins]
+int ref_error_report(const float* x, const float* y, uint64_t n, uint32_t bins, double* out8, uint64_t* counts) {
+    return guarded([&] {
+        auto r = taco::error_report(std::span<const float>(x, n), std::span<const float>(y, n), bins);
+        out8[0] = r.mse;
+        out8[1] = r.relative_l2;
+        out8[2] = r.max_abs_error;
+        out8[3] = r.zero_collapse_fraction;
+        out8[4] = r.kurtosis;
+        out8[5] = r.kurtosis_defined ? 1.0 : 0.0;
+        out8[6] = r.histogram.bin_edges.front();
+        out8[7] = r.histogram.bin_edges.back();
+        for (uint32_t i = 0; i < bins; ++i) counts[i] = r.histogram.counts[i];
+    });
+}
+
 uint8_t ref_fp8_encode(float x, int fmt) {
     return taco::fp8_encode(x, fmt ? taco::Fp8Format::e5m2() : taco::Fp8Format::e4m3());
 }

@@ -50,6 +50,14 @@ class Config(C.Structure):
                 f"direct_scale={self.direct_scale})")
 
 
+class ErrorReportC(C.Structure):
+    """taco_error_report == taco::ErrorReport (analysis.hpp:18-26) without the histogram vectors."""
+
+    _fields_ = [("mse", C.c_double), ("relative_l2", C.c_double), ("max_abs_error", C.c_double),
+                ("zero_collapse_fraction", C.c_double), ("kurtosis", C.c_double), ("kurtosis_defined", C.c_int),
+                ("hist_lo", C.c_double), ("hist_hi", C.c_double)]
+
+
 class Layout(C.Structure):
     _fields_ = [("nblocks", C.c_uint64), ("codes_bytes", C.c_uint64), ("scal_offset", C.c_uint64),
                 ("msg_bytes", C.c_uint64), ("msg_stride", C.c_uint64)]
@@ -90,6 +98,7 @@ _SIGNATURES = {
     "taco_archive_parse_header": (C.c_int, [_P, _U64, C.POINTER(Config), C.POINTER(C.c_uint64)]),
     "taco_archive_import_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P, _P]),
     "taco_scaled_spectrum_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P]),
+    "taco_error_report_dev": (C.c_int, [_P, _I, _P, _I, _U64, _U32, C.POINTER(ErrorReportC), _P, _P]),
     "taco_fp8_encode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
     "taco_fp8_decode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
 }

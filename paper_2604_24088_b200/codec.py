@@ -216,6 +216,26 @@ def _scan_scalars(raw, cfg: Config, complete: int) -> None:
             raise TacoError(_abi.ERR_CORRUPT, "block scalars must be finite")
 
 
+def error_report(original: torch.Tensor, reconstructed: torch.Tensor, bins: int = 64, stream=None) -> dict:
+    """taco::error_report (analysis.hpp:42) on the device: mse, relative_l2, max_abs_error,
+    zero_collapse_fraction, kurtosis (excess, of the elementwise error), histogram."""
+    _require_cuda(original, reconstructed)
+    x, y = original.reshape(-1).contiguous(), reconstructed.reshape(-1).contiguous()
+    if x.numel() != y.numel():
+        raise TacoError(_abi.ERR_INPUT, "original and reconstructed lengths differ")
+    rep = _abi.ErrorReportC()
+    counts = (C.c_uint64 * max(bins, 1))()
+    _abi.check(_abi.lib().taco_error_report_dev(_ptr(x), _dtype_code(x.dtype), _ptr(y), _dtype_code(y.dtype),
+                                                x.numel(), bins, C.byref(rep), C.cast(counts, C.c_void_p),
+                                                C.c_void_p(_stream(stream))))
+    width = (rep.hist_hi - rep.hist_lo) / bins
+    edges = [rep.hist_lo + width * i for i in range(bins)] + [rep.hist_hi]
+    return {"mse": rep.mse, "relative_l2": rep.relative_l2, "max_abs_error": rep.max_abs_error,
+            "zero_collapse_fraction": rep.zero_collapse_fraction,
+            "kurtosis": rep.kurtosis if rep.kurtosis_defined else float("nan"),
+            "kurtosis_defined": bool(rep.kurtosis_defined), "bin_edges": edges, "counts": list(counts)}
+
+
 def split_message(msg: torch.Tensor, cfg: Config, nblocks: int):
     """(codes [nblocks*payload] uint8, alpha [nblocks] f32, scale [nblocks] f32) views of one message."""
     lay = _abi.msg_layout(cfg, nblocks)

@@ -359,6 +359,28 @@ int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, u
     return TACO_OK;
 }
 
+int taco_error_report_dev(const void* original, int orig_dtype, const void* reconstructed, int recon_dtype,
+                          uint64_t n, uint32_t bins, taco_error_report* out, uint64_t* counts, void* stream) {
+    if (int rc = check_dtype(orig_dtype)) return rc;
+    if (int rc = check_dtype(recon_dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (bins == 0) return fail(TACO_ERR_CONFIG, "histogram needs at least one bin");
+    double r[8];
+    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "");
+    if (int e = taco_impl::error_report_dev(original, orig_dtype, reconstructed, recon_dtype, n, bins, r,
+                                            reinterpret_cast<unsigned long long*>(counts), (cudaStream_t)stream))
+        return cuda_fail((cudaError_t)e, "error report");
+    out->mse = r[0];
+    out->relative_l2 = r[1];
+    out->max_abs_error = r[2];
+    out->zero_collapse_fraction = r[3];
+    out->kurtosis = r[4];
+    out->kurtosis_defined = r[5] != 0.0;
+    out->hist_lo = r[6];
+    out->hist_hi = r[7];
+    return TACO_OK;
+}
+
 // ------------------------------------------------ TACOCMP1 archive (serialize.cpp) ----
 // magic "TACOCMP1", kind u8, format id u8, block size u32 LE, length u64 LE, then per
 // block [payload][alpha f32][scale f32] (serialize.cpp:109-124).

@@ -57,6 +57,10 @@ cudaError_t launch_decompress_kind(const Launch& l, const taco_dev::ShardArgs& a
 cudaError_t launch_scaled_spectrum(const Launch& l, const taco_dev::ShardArgs& a, const taco_dev::CodecConsts& c,
                                    double qtop);
 cudaError_t launch_add_f32(float* acc, const float* x, uint64_t n, cudaStream_t stream);
+// analysis error_report on the device (synchronous; out8 = mse, relative_l2, max_abs,
+// zero_collapse, kurtosis, kurtosis_defined, hist lo, hist hi); returns a cudaError_t
+int error_report_dev(const void* x, int dx, const void* y, int dy, uint64_t n, uint32_t bins, double* out8,
+                     unsigned long long* counts_host, cudaStream_t st);
 // mode 0: SoA message -> TACOCMP1 archive (header from hdr22); mode 1: archive body -> message
 cudaError_t launch_archive(const uint8_t* src, uint8_t* dst, uint64_t nblocks, uint64_t payload, uint64_t scal_off,
                            const uint8_t* hdr22, int mode, int* flags, cudaStream_t stream);

@@ -120,3 +120,26 @@ def test_nccl_schedule_world1(port, nccl_world1):
     torch.cuda.synchronize()
     assert torch.equal(out, y1)
     assert COLLECTIVE_RELMSE_MAX > 0
+
+
+def test_tp_regions_and_custom_ops_on_gpu(port, nccl_world1):
+    """tp.py on the CUDA codec (world size 1: the two-shot degenerates to a round trip) and the
+    torch.library ops taco_b200::compress / decompress."""
+    from paper_2604_24088_b200 import tp
+
+    cfg = make_config(256)
+    ctx = tp.TpContext(cfg=cfg, chunks=2)
+    T, H, F = 256, 512, 384
+    x = torch.from_numpy(port.mixture(T * F, 3).reshape(T, F)).cuda().to(torch.bfloat16).requires_grad_(True)
+    row = tp.RowParallelLinear(F, H, ctx, device="cuda", dtype=torch.bfloat16)
+    y = row(x)
+    local = torch.nn.functional.linear(x.detach(), row.linear.weight.detach())
+    rt = codec.decompress(codec.compress(local, cfg), local.numel(), cfg, out_dtype=torch.bfloat16).view(T, H)
+    assert torch.equal(y.detach(), rt)
+    y.float().sum().backward()
+    assert x.grad is not None and torch.isfinite(x.grad.float()).all()
+    # torch.library ops == the direct device API
+    msg = torch.ops.taco_b200.compress(local, 256, 0)
+    assert torch.equal(msg, codec.compress(local, cfg)[0])
+    back = torch.ops.taco_b200.decompress(msg, local.numel(), 256, 0, torch.float32)
+    assert torch.equal(back, codec.decompress(codec.compress(local, cfg), local.numel(), cfg))

@@ -162,3 +162,29 @@ def test_archive_errors_match_reference(port):
         with pytest.raises(TacoError, match=msg) as ei:
             imp(raw)
         assert ei.value.code == "corrupt"
+
+
+# --------------------------------------------------------- error metrics (§8 f4) ---
+@pytest.mark.parametrize("bins", [1, 64])
+def test_error_report_matches_reference(ref, port, bins):
+    x = port.mixture(1_000_003, 7)
+    cfg = make_config(256)
+    xd = torch.from_numpy(x).cuda()
+    y = codec.decompress(codec.compress(xd, cfg), x.size, cfg)
+    got = codec.error_report(xd, y, bins)
+    want = ref.error_report(x, y.cpu().numpy(), bins)
+    for k in ("mse", "relative_l2", "kurtosis"):  # sums in another order: last-bit differences
+        assert got[k] == pytest.approx(want[k], rel=1e-9), k
+    assert got["max_abs_error"] == want["max_abs_error"]
+    assert got["zero_collapse_fraction"] == want["zero_collapse_fraction"]
+    assert got["bin_edges"][0] == want["lo"] and got["bin_edges"][-1] == want["hi"]
+    assert got["counts"] == want["counts"]
+
+
+def test_error_report_edge_cases():
+    z = torch.zeros(1000, device="cuda")
+    r = codec.error_report(z, z, 8)
+    assert r["mse"] == 0.0 and r["relative_l2"] == 0.0 and not r["kurtosis_defined"]
+    assert r["bin_edges"][0] == -0.5 and r["bin_edges"][-1] == 0.5 and r["counts"][4] == 1000
+    with pytest.raises(TacoError, match="input tensor is empty"):
+        codec.error_report(torch.zeros(0, device="cuda"), torch.zeros(0, device="cuda"))
