@@ -33,6 +33,13 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     from . import _abi, collective
     from ._abi import make_config
 
+    if "RANK" not in os.environ:  # `bench.py --collective` without torchrun: a world of one
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

@@ -134,8 +134,10 @@ def test_tp_regions_and_custom_ops_on_gpu(port, nccl_world1):
     row = tp.RowParallelLinear(F, H, ctx, device="cuda", dtype=torch.bfloat16)
     y = row(x)
     local = torch.nn.functional.linear(x.detach(), row.linear.weight.detach())
-    rt = codec.decompress(codec.compress(local, cfg), local.numel(), cfg, out_dtype=torch.bfloat16).view(T, H)
-    assert torch.equal(y.detach(), rt)
+    # world size 1: the two-shot is K1 -> K3 (decode, re-encode) -> K2, a double round trip
+    rt1 = codec.decompress(codec.compress(local, cfg), local.numel(), cfg)
+    rt2 = codec.decompress(codec.compress(rt1, cfg), local.numel(), cfg).view(T, H)
+    assert rel_mse(y.detach().float().cpu().numpy(), rt2.cpu().numpy()) < 1e-5  # bf16 output rounding
     y.float().sum().backward()
     assert x.grad is not None and torch.isfinite(x.grad.float()).all()
     # torch.library ops == the direct device API
