@@ -81,7 +81,10 @@ struct FastDiv {
 };
 
 constexpr int kPipeWarps = 4;    // warps per CTA of the persistent kernels
-constexpr int kPipeMinCtas = 4;  // >= 16 resident warps per SM (caps registers at 128)
+#ifndef TACO_PIPE_MIN_CTAS
+#define TACO_PIPE_MIN_CTAS 4
+#endif
+constexpr int kPipeMinCtas = TACO_PIPE_MIN_CTAS;  // 4: >= 16 resident warps per SM (caps registers at 128)
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);

@@ -49,8 +49,12 @@ constexpr int kSlab = kM * 128;      // one 64-element K slab of the tile: 128 r
 constexpr int kStageBytes = 4 * kSlab;  // 64 KB: the whole 128 x 256 bf16 tile
 constexpr int kBBytes = 64 * 128;    // H64: 64 rows (n) x 64 k x bf16 = one K slab
 constexpr int kBufs = 2;             // TMEM accumulator buffers
-constexpr int kEpiWarps = 16;        // 2 groups (one per TMEM buffer) x 4 lane quarters x 2 column halves
-constexpr int kGroupWarps = kEpiWarps / kBufs;
+#ifndef TACO_TC_GROUPS
+#define TACO_TC_GROUPS 2
+#endif
+constexpr int kEpiGroups = TACO_TC_GROUPS;  // epilogue groups: group g takes tiles i = g mod groups
+constexpr int kGroupWarps = 8;              // 4 lane quarters x 2 column halves
+constexpr int kEpiWarps = kEpiGroups * kGroupWarps;
 constexpr int kSsWarps = 4;          // sum-of-squares warps: one thread per block row
 constexpr int kEpi0 = 2 + kSsWarps;  // first epilogue warp
 constexpr int kThreads = (kEpi0 + kEpiWarps) * 32;
@@ -61,8 +65,8 @@ struct Smem {  // byte offsets inside the 1024-aligned dynamic shared memory
     static constexpr int B = A + kStages * kStageBytes;
     static constexpr int SS = B + kBBytes;               // [2 parity][128 rows] double: sum of squares
     static constexpr int AL = SS + 2 * kM * 8;           // [2 parity][128 rows] float: alpha
-    static constexpr int RED_MX = AL + 2 * kM * 4;       // [2 parity][4 cg][128 rows] float
-    static constexpr int BARS = RED_MX + 2 * 4 * kM * 4; // full, empty [kStages]; tfull, tempty, ssfull, ssempty [kBufs]
+    static constexpr int RED_MX = AL + 2 * kM * 4;       // [groups][2][2 halves][128 rows] float
+    static constexpr int BARS = RED_MX + kEpiGroups * 2 * 2 * kM * 4; // full, empty [kStages]; tfull, tempty, ssfull, ssempty [kBufs]
     static constexpr int TMEM = BARS + (2 * kStages + 4 * kBufs) * 8;
     static constexpr int TOTAL = TMEM + 16;
 };
@@ -386,14 +390,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float2 neg1 = make_float2(-1.0f, -1.0f);
         uint32_t i = grp;
         uint32_t t = blockIdx.x + grp * gridDim.x;
-        for (; t < ntiles; t += kBufs * gridDim.x, i += kBufs) {
-            const int pp = (i >> 1) & 1;
+        for (; t < ntiles; t += kEpiGroups * gridDim.x, i += kEpiGroups) {
+            const int pp = (i / kEpiGroups) & 1, buf = i % kBufs, par = i & 1;
             const uint32_t p = tps.div(t);
             const uint64_t kk = (uint64_t)(t - p * tps.d) * kM + r;  // block within the chunk
             const bool live = kk < a.nblk;
-            mbar_wait_u(bar_tfull + 8 * grp, (i >> 1) & 1);
+            mbar_wait_u(bar_tfull + 8 * buf, (i / kBufs) & 1);
             tc_fence_after();
-            const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16) + grp * 256 + h * 32;
+            const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16) + buf * 256 + h * 32;
             float mx = 0.0f;
 #pragma unroll
             for (int sub = 0; sub < 4; ++sub) {  // 8 columns at a time: P0..P3 in 32 registers
@@ -418,11 +422,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             red[h * kM + r] = mx;
             named_bar(1 + grp * 4 + quarter, 64);
             const float ymax = fmaxf(red[r], red[kM + r]);
-            mbar_wait_u(bar_ssfull + 8 * grp, (i >> 1) & 1);
-            const double ss = ss_buf[grp * kM + r];
-            const float alpha = al_buf[grp * kM + r];
+            mbar_wait_u(bar_ssfull + 8 * par, (i >> 1) & 1);
+            const double ss = ss_buf[par * kM + r];
+            const float alpha = al_buf[par * kM + r];
             __syncwarp();
-            if (lane == 0) mbar_arrive_u(bar_ssempty + 8 * grp);
+            if (lane == 0) mbar_arrive_u(bar_ssempty + 8 * par);
             uint8_t* m = msgs + p * a.msg_stride;
             const bool overflow = !isfinite(ymax) && isfinite(ss);
             float s_blk;
@@ -471,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_u(bar_tempty + 8 * grp);
+            if (lane == 0) mbar_arrive_u(bar_tempty + 8 * buf);
             if (live && !overflow && !(TACO_TC_DEBUG & 2)) {
                 uint8_t* cp = m + kk * kB + h * 32;
                 if ((reinterpret_cast<uintptr_t>(m) & 31) == 0) {  // messages past the first may be 16-aligned only
