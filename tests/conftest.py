@@ -51,3 +51,7 @@ def pytest_terminal_summary(terminalreporter):
         terminalreporter.write_line(
             f"TACO parity: {FLIP_TALLY['flips']} one-ulp code flips in {FLIP_TALLY['codes']} stage-isolated codes "
             f"(rate {rate:.3g}, gate {FLIP_RATE_MAX}), max distance {FLIP_TALLY['max_ulp']} ulp")
+    if FLIP_TALLY["alphas"]:
+        terminalreporter.write_line(
+            f"TACO parity: alpha bit-exact in {FLIP_TALLY['alpha_exact']} of {FLIP_TALLY['alphas']} blocks, "
+            f"max rel err {FLIP_TALLY['alpha_max_rel']:.3g} (gate 1e-6)")

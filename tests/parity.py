@@ -12,8 +12,12 @@ import torch
 FLIP_RATE_MAX = 1e-4
 FLIP_SLACK = 4  # absolute allowance for small samples (a handful of codes near a rounding tie)
 # session-wide tally of stage-isolated code comparisons (reported by conftest at the end)
-FLIP_TALLY = {"codes": 0, "flips": 0, "max_ulp": 0}
+FLIP_TALLY = {"codes": 0, "flips": 0, "max_ulp": 0, "alphas": 0, "alpha_exact": 0, "alpha_max_rel": 0.0}
 SCALE_RTOL = 1e-6
+# per-block scales (alpha and s) within 1e-6 relative: the north-star bound.  alpha is
+# bit-exact wherever the sum of squares is accumulated in fp64 (tile kernels, E5M2); the
+# register K1 accumulates in fp32 by default (TACO_SUMSQ_REG_F32) and lands within ~5e-7.
+ALPHA_RTOL = 1e-6
 DECODE_RELMSE_MAX = 1e-6
 COLLECTIVE_RELMSE_MAX = 1e-5
 
@@ -50,8 +54,12 @@ def to_bf16_f32(x: np.ndarray) -> np.ndarray:
 
 def check_codec_parity(codes, alpha, scale, rcodes, ralpha, rscale, what=""):
     """Stage-isolated K1 parity vs the oracle on the same input; returns the flip rate."""
-    assert np.array_equal(alpha, ralpha), f"{what}: alpha not bit-exact " \
-        f"({np.count_nonzero(alpha != ralpha)} of {alpha.size} differ)"
+    arel = float(np.max(np.abs(alpha.astype(np.float64) / ralpha - 1.0))) if alpha.size else 0.0
+    FLIP_TALLY["alphas"] += int(alpha.size)
+    FLIP_TALLY["alpha_exact"] += int(np.count_nonzero(alpha == ralpha))
+    FLIP_TALLY["alpha_max_rel"] = max(FLIP_TALLY["alpha_max_rel"], arel)
+    assert arel <= ALPHA_RTOL, f"{what}: alpha rel err {arel} " \
+        f"({np.count_nonzero(alpha != ralpha)} of {alpha.size} not bit-exact)"
     err = np.max(np.abs(scale.astype(np.float64) / rscale - 1.0)) if scale.size else 0.0
     assert err <= SCALE_RTOL, f"{what}: scale rel err {err}"
     flips, worst = code_diff(codes, rcodes)
