@@ -12,6 +12,10 @@
 
 #include "taco_device.cuh"
 
+#ifndef TACO_FAST_SCALARS_REG
+#define TACO_FAST_SCALARS_REG 1  // branch-free scalar chain (+2.5 % K1, profiles/README.md)
+#endif
+
 namespace taco_dev {
 
 struct ShardArgs {
@@ -48,7 +52,11 @@ __device__ __forceinline__ int clamp_valid(int64_t a, int64_t b, int B) {
 template <int L, typename R>
 __device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, float& alpha, float& s, double& ss) {
     ss = group_sum<L>(v.sumsq());
+#if TACO_FAST_SCALARS_REG
+    alpha = block_alpha_fast(ss, c);
+#else
     alpha = block_alpha(ss, c);
+#endif
     // Exact power-of-two pre-scale, only where the butterfly could overflow fp32
     // (|y| <= B*max|x| <= B*sqrt(ss)); elsewhere p2 = 1 and the multiply is skipped.
     const bool huge = !(ss < 0x1p160);
@@ -62,7 +70,11 @@ __device__ __forceinline__ void quantise(R& v, int q, const CodecConsts& c, floa
 #pragma unroll
     for (int m = 1; m < L; m <<= 1) ymax = fmax(ymax, __shfl_xor_sync(kFull, ymax, m));
     double k;
+#if TACO_FAST_SCALARS_REG
+    block_scale_fast((double)ymax, alpha, p2, c, s, k);
+#else
     block_scale((double)ymax, alpha, p2, c, s, k);
+#endif
     v.mul(k);
 }
 

@@ -261,7 +261,11 @@ template <int NB>
 __device__ __forceinline__ void tile_quantise(float2 (&w)[TG<NB>::E2], double ss, float p2, const CodecConsts& c,
                                               float& alpha, float& s) {
     using Gm = TG<NB>;
+#if TACO_FAST_SCALARS_REG
+    alpha = block_alpha_fast(ss, c);
+#else
     alpha = block_alpha(ss, c);
+#endif
     float m[Gm::E2];
 #pragma unroll
     for (int i = 0; i < Gm::E2; ++i) m[i] = fmaxf(fabsf(w[i].x), fabsf(w[i].y));
@@ -273,7 +277,11 @@ __device__ __forceinline__ void tile_quantise(float2 (&w)[TG<NB>::E2], double ss
 #pragma unroll
     for (int o = 1; o < kLanes; o <<= 1) ymax = fmaxf(ymax, __shfl_xor_sync(kFull, ymax, o));
     double k;
+#if TACO_FAST_SCALARS_REG
+    block_scale_fast((double)ymax, alpha, p2, c, s, k);
+#else
     block_scale((double)ymax, alpha, p2, c, s, k);
+#endif
     mul_wide<Gm::E2>(w, k);
 }
 
