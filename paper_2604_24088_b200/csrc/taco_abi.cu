@@ -226,6 +226,7 @@ int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(x) && (shards == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a, b);
     Launch l{cfg->block_size, dtype, (int)cfg->format, x, msgs, nullptr, (cudaStream_t)stream};
     if (cfg->kind != 0) {
         uint32_t* smax = taco_impl::claim_scratch(shards);
@@ -251,6 +252,7 @@ int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_s
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(out) && (shards == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a, b);
     Launch l{cfg->block_size, out_dtype, (int)cfg->format, msgs, out, nullptr, (cudaStream_t)stream};
     if (cfg->kind != 0) {
         if (cudaError_t e = taco_impl::launch_decompress_kind(l, a, consts_of(cfg), (int)cfg->kind))
@@ -279,6 +281,8 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     if (nranks > 1 && rank_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
                 acc_out ? aligned16(acc_out) : 0, d_flags};
+    taco_dev::with_full_blocks(a, b);
+    a.full_last = a.full_mid;  // every rank's message covers the same (single) shard
     Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, out_msg, acc_out, (cudaStream_t)stream};
     if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
         return cuda_fail(e, "K3 reduce-encode launch");
@@ -352,6 +356,7 @@ int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, u
     if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
     const uint64_t b = cfg->block_size, m = div_up(n, b);
     ShardArgs a{n, n, 1, 0, m, 0, 0, 0, d_flags};
+    taco_dev::with_full_blocks(a, b);
     Launch l{cfg->block_size, dtype, (int)cfg->format, x, out, nullptr, (cudaStream_t)stream};
     const double qtop = cfg->kind == 4 ? 127.0 : (cfg->format ? 57344.0 : 448.0);  // codec.cpp:311-313
     if (cudaError_t e = taco_impl::launch_scaled_spectrum(l, a, consts_of(cfg), qtop))

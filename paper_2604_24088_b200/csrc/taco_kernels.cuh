@@ -28,7 +28,21 @@ struct ShardArgs {
     uint64_t scal_off;    // byte offset of the (alpha, s) array in a message
     int vec_ok;           // element pointers allow V-wide vector access
     int* flags;           // device error flags (may be null)
+    // leading blocks of the chunk that are whole (no shard / tensor tail) in a shard other
+    // than the last and in the last one (host-computed by with_full_blocks)
+    uint64_t full_mid = 0, full_last = 0;
 };
+
+// number of whole blocks of a chunk; every kernel's "is this tile full" is one compare
+__host__ __device__ inline void with_full_blocks(ShardArgs& a, uint64_t B) {
+    auto whole = [&](uint64_t valid) -> uint64_t {
+        const uint64_t wb = valid / B;
+        return wb <= a.blk0 ? 0 : (wb - a.blk0 < a.nblk ? wb - a.blk0 : a.nblk);
+    };
+    const uint64_t last_valid = a.P == 0 ? 0 : (a.n > (uint64_t)(a.P - 1) * a.S ? a.n - (uint64_t)(a.P - 1) * a.S : 0);
+    a.full_mid = whole(a.S);
+    a.full_last = whole(last_valid < a.S ? last_valid : a.S);
+}
 
 constexpr int kWarpThreads = 256;  // 8 warps per CTA
 constexpr int kBigThreads = 512;   // one block per CTA for B >= 2048
@@ -117,12 +131,11 @@ __device__ __forceinline__ void unpack16(const uint4 u, float2* out) {
     }
 }
 
-// tile -> (shard, first block) and whether the whole tile is full and vector-aligned
+// whether the G blocks of a tile starting at block kk0 of shard p are all whole and the
+// element pointers allow vector access
 template <int B, int G>
 __device__ __forceinline__ bool tile_full(const ShardArgs& a, uint64_t p, uint64_t kk0) {
-    if (!a.vec_ok || kk0 + G > a.nblk) return false;
-    const uint64_t end = (a.blk0 + kk0 + G) * B;  // one past the tile, within the shard
-    return end <= a.S && p * a.S + end <= a.n;
+    return a.vec_ok && kk0 + G <= (p + 1 == a.P ? a.full_last : a.full_mid);
 }
 
 template <int B, typename TIn, int FMT, int EMAX, int VMAX>

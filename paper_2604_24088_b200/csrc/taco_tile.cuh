@@ -541,7 +541,13 @@ __device__ __forceinline__ bool tile_decode(const uint8_t* codes, float2 sc, flo
     } else {
         stages<Gm::E2, Gm::LO - 1, Gm::LO + 2>(w);
     }
+#if TACO_FAST_SCALARS_REG
+    // s * norm / alpha with a Newton reciprocal (2 steps: the float rounding of the
+    // multiplier matches the correctly rounded quotient except in double-rounding cases)
+    mul_wide<Gm::E2>(w, (double)sc.y * c.norm * rcp_newton((double)sc.x, 2));
+#else
     mul_wide<Gm::E2>(w, block_dequant(sc.x, sc.y, c));
+#endif
     return scalars_ok(sc.x, sc.y);
 }
 
@@ -645,8 +651,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         const uint64_t kk = kk0 + g;
         if (q == 0 && kk < a.nblk && !ok) raise_flag(a.flags, 2);
         // whole tile valid and vector-aligned -> staged, coalesced 128-bit stores
-        const bool full = a.vec_ok && kk0 + kBlocks <= a.nblk &&
-                          (a.blk0 + kk0 + kBlocks) * B <= a.S && p * a.S + (a.blk0 + kk0 + kBlocks) * B <= a.n;
+        const bool full = tile_full<B, kBlocks>(a, p, kk0);
         TOut* dst = out + (p * a.S + (a.blk0 + kk0) * B);
         if (__all_sync(kFull, full)) {
             __syncwarp();
