@@ -11,7 +11,10 @@ template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
-        if (kernel_family() != 2) {
+        // measured (profiles/README.md): tile kernels for B >= 256 and fp32 output at
+        // B = 128; the register kernel (K2_EMAX lanes geometry) at B = 64 and bf16 B = 128
+        const bool tile = B >= 256 || (B == 128 && std::is_same<T, float>::value);
+        if (kernel_family() != 2 && (tile || kernel_family() == 1)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K2T<NB, T>;
             const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;

@@ -10,7 +10,7 @@ namespace {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0) return cudaSuccess;
-    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+    if constexpr (FMT == 0 && B >= 256 && B <= 512) {
         if (kernel_family() != 2) {  // K2's decode is the tile kernel: decode with the same code
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K3T<NB>;
