@@ -682,16 +682,57 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
 // Owner step of the two-shot (collective.cpp:95-101): decode the P ranks' copies of a
 // tile with tile_decode (so every rank's slice is bit-identical to what K2 produces),
 // sum in fp32 in ascending rank order, zero the positions past the shard end, then
-// re-encode with the K1 tile path.  One warp per tile; plain coalesced loads (the P
-// messages are small per tile and come from the all-to-all receive buffer).
+// re-encode with exactly K1's fp32 operations (so the result equals compress(sum), the
+// property test_collective.cpp:123-156 pins).  The sum goes from the decode's phase-2
+// registers to K1's phase-1 registers through one swizzled transpose (no natural-order
+// round trip).  One warp per tile; the next rank's codes and scalars are prefetched into
+// registers while the current rank is decoded.
 template <int NB>
 struct K3T {
     using Gm = TG<NB>;
-    static constexpr int SLOT = Gm::TILE * 4;  // fp32 tile; also holds codes + scalars
+    static constexpr int SLOT = Gm::TILE + kBlocks * 8;  // codes + scalars of one rank's tile
     static constexpr int XB = Gm::TILE * 4;
     static constexpr int WARP_BYTES = SLOT + XB;
     static constexpr size_t SMEM = (size_t)kTileWarps * WARP_BYTES;
+    static constexpr int CHUNKS = Gm::TILE / 16;         // 16-byte code chunks per tile
+    static constexpr int PER_LANE = (CHUNKS + 31) / 32;
 };
+
+// phase-2 registers -> fp32 tile buffer (the inverse of xpose_read), and the phase-1 read
+// back (the inverse of xpose_write): same swizzle, so both directions stay conflict-free
+template <int NB>
+__device__ __forceinline__ void xpose_write2(float* xb, const float2 (&w)[TG<NB>::E2], int g, int q) {
+    using Gm = TG<NB>;
+    const uint32_t p0 = (uint32_t)(g * Gm::B + Gm::pos2(0, q));
+    const uint32_t kl = swz(p0 >> 2);
+    if constexpr (Gm::VW >= 4) {
+#pragma unroll
+        for (int c = 0; c < Gm::E / 4; ++c) {
+            const uint32_t kr = swz((uint32_t)Gm::pos2(4 * c, 0) >> 2);
+            *reinterpret_cast<float4*>(xb + 4 * (kl ^ kr)) =
+                make_float4(w[2 * c].x, w[2 * c].y, w[2 * c + 1].x, w[2 * c + 1].y);
+        }
+    } else {
+#pragma unroll
+        for (int r = 0; r < Gm::E; ++r) {
+            const uint32_t pr = (uint32_t)Gm::pos2(r, 0);
+            xb[4 * (kl ^ swz(pr >> 2)) + ((p0 | pr) & 3)] = (r & 1) ? w[r / 2].y : w[r / 2].x;
+        }
+    }
+}
+
+template <int NB>
+__device__ __forceinline__ void xpose_read1(const float* xb, float2 (&w)[TG<NB>::E2], int g, int q) {
+    using Gm = TG<NB>;
+    const uint32_t kl = swz((uint32_t)(g * Gm::B + Gm::pos1(0, q)) >> 2);
+#pragma unroll
+    for (int c = 0; c < Gm::E / 4; ++c) {
+        const uint32_t kr = swz((uint32_t)Gm::pos1(4 * c, 0) >> 2);
+        const float4 v = *reinterpret_cast<const float4*>(xb + 4 * (kl ^ kr));
+        w[2 * c] = make_float2(v.x, v.y);
+        w[2 * c + 1] = make_float2(v.z, v.w);
+    }
+}
 
 template <int NB, typename TAcc>
 __global__ void __launch_bounds__(kTileWarps * 32)
@@ -711,21 +752,34 @@ __global__ void __launch_bounds__(kTileWarps * 32)
     const bool live = kk < a.nblk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)((a.blk0 + kk) * B), (int64_t)B, B) : 0;
 
+    // rank r's codes + scalars of this tile, in registers (prefetched one rank ahead)
+    uint4 pre[Cf::PER_LANE];
+    float2 pre_sc = make_float2(1.0f, 1.0f);
+    auto fetch = [&](uint32_t r) {
+        const uint8_t* m = msgs + r * a.msg_stride;
+#pragma unroll
+        for (int h = 0; h < Cf::PER_LANE; ++h) {
+            const int i = lane + 32 * h;
+            const bool bl = i < Cf::CHUNKS && kk0 + (uint64_t)((16 * i) >> NB) < a.nblk;
+            pre[h] = bl ? __ldg(reinterpret_cast<const uint4*>(m + kk0 * B + 16 * (uint64_t)i)) : make_uint4(0, 0, 0, 0);
+        }
+        if (lane < kBlocks)
+            pre_sc = kk0 + lane < a.nblk ? __ldg(reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + lane) * 8))
+                                         : make_float2(1.0f, 1.0f);
+    };
+    fetch(0);
     float2 acc[Gm::E2];
     bool ok = true;
     for (uint32_t r = 0; r < a.P; ++r) {
-        const uint8_t* m = msgs + r * a.msg_stride;
         __syncwarp();  // previous rank's slot contents fully consumed
-        for (int i = lane; i < Gm::TILE / 16; i += 32) {
-            const bool bl = kk0 + (uint64_t)((16 * i) >> NB) < a.nblk;
-            reinterpret_cast<uint4*>(slot)[i] =
-                bl ? *reinterpret_cast<const uint4*>(m + kk0 * B + 16 * (uint64_t)i) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int h = 0; h < Cf::PER_LANE; ++h) {
+            const int i = lane + 32 * h;
+            if (i < Cf::CHUNKS) reinterpret_cast<uint4*>(slot)[i] = pre[h];
         }
-        if (lane < kBlocks)
-            reinterpret_cast<float2*>(slot + Gm::TILE)[lane] =
-                kk0 + lane < a.nblk ? *reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + lane) * 8)
-                                    : make_float2(1.0f, 1.0f);
+        if (lane < kBlocks) reinterpret_cast<float2*>(slot + Gm::TILE)[lane] = pre_sc;
         __syncwarp();
+        if (r + 1 < a.P) fetch(r + 1);
         const float2 sc = reinterpret_cast<const float2*>(slot + Gm::TILE)[g];
         float2 w[Gm::E2];
         ok &= tile_decode<NB>(slot, sc, xb, w, g, q, c);
@@ -739,43 +793,79 @@ __global__ void __launch_bounds__(kTileWarps * 32)
     }
     // positions past the shard end are padding of the re-encoded slice (collective.cpp:101)
 #pragma unroll
-    for (int r = 0; r < Gm::E; ++r) {
-        if (Gm::pos2(r, q) >= valid) {
-            if (r & 1) acc[r / 2].y = 0.0f;
-            else acc[r / 2].x = 0.0f;
+    for (int rr = 0; rr < Gm::E; ++rr) {
+        if (Gm::pos2(rr, q) >= valid) {
+            if (rr & 1) acc[rr / 2].y = 0.0f;
+            else acc[rr / 2].x = 0.0f;
         }
     }
     if (live && acc_out) {
         TAcc* dst = acc_out + (a.blk0 + kk) * B;
 #pragma unroll
-        for (int r = 0; r < Gm::E; ++r) {
-            const int pos = Gm::pos2(r, q);
-            if (pos < valid) store_one(dst + pos, (r & 1) ? acc[r / 2].y : acc[r / 2].x);
+        for (int rr = 0; rr < Gm::E; ++rr) {
+            const int pos = Gm::pos2(rr, q);
+            if (pos < valid) store_one(dst + pos, (rr & 1) ? acc[rr / 2].y : acc[rr / 2].x);
         }
     }
     if (out_msg == nullptr) {  // reduce-scatter: the fp32 sum is the product
         if (live && q == 0 && !ok) raise_flag(a.flags, 2);
         return;
     }
-    // natural-order fp32 tile for the encoder
+    // ---- re-encode: exactly K1's operations on an fp32 tile (tile_rotate<NB, float>), with
+    // the tile taken from registers instead of a natural-order load
+    __syncwarp();  // xb free (the last tile_decode read it)
+    xpose_write2<NB>(xb, acc, g, q);
     __syncwarp();
-    float* nat = reinterpret_cast<float*>(slot);
-#pragma unroll
-    for (int r = 0; r < Gm::E; ++r) nat[g * B + Gm::pos2(r, q)] = (r & 1) ? acc[r / 2].y : acc[r / 2].x;
-    __syncwarp();
-    float2 w[Gm::E2];
+    xpose_read1<NB>(xb, acc, g, q);  // phase-1 registers: tile_rotate's raw words
     double ss;
-    float p2;
-    tile_rotate<NB, float>(slot, xb, w, g, q, c, ss, p2);
+    float p2 = 1.0f;
+    {
+        double d4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int i = 0; i < Gm::E2; ++i) {
+            const double d0 = (double)acc[i].x, d1 = (double)acc[i].y;
+            d4[(2 * i) & 3] = fma(d0, d0, d4[(2 * i) & 3]);
+            d4[(2 * i + 1) & 3] = fma(d1, d1, d4[(2 * i + 1) & 3]);
+        }
+        const double sl = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+        ss = sl;
+#pragma unroll
+        for (int o = 1; o < kLanes; o <<= 1) ss += __shfl_xor_sync(kFull, ss, o);
+        if (__any_sync(kFull, !(sl < 0x1p150))) {
+            p2 = pow2_near(block_alpha(ss, c));
+#pragma unroll
+            for (int i = 0; i < Gm::E2; ++i) {
+                const float x0 = acc[i].x * p2, x1 = acc[i].y * p2;
+                acc[i] = make_float2(x0 + x1, x0 - x1);
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < Gm::E2; ++i) acc[i] = make_float2(acc[i].x + acc[i].y, acc[i].x - acc[i].y);
+        }
+    }
+    stages_rev<Gm::E2, 0, Gm::NE - 1>(acc);
+    __syncwarp();
+    xpose_write<NB>(xb, acc, g, q);
+    __syncwarp();
+    xpose_read<NB>(xb, acc, g, q);
+    if constexpr (Gm::LO == 0) {
+        pair_stage<Gm::E2>(acc);
+        stages<Gm::E2, 0, 2>(acc);
+    } else {
+        stages<Gm::E2, Gm::LO - 1, Gm::LO + 2>(acc);
+    }
     float alpha, s;
-    tile_quantise<NB>(w, ss, p2, c, alpha, s);
+    tile_quantise<NB>(acc, ss, p2, c, alpha, s);
     __syncwarp();
     uint8_t* cb = reinterpret_cast<uint8_t*>(xb);
-    stage_codes<NB>(cb, w, g, q);
+    stage_codes<NB>(cb, acc, g, q);
     __syncwarp();
-    for (int j = lane; j < Gm::TILE / 16; j += 32) {
-        const uint4 v = *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
-        if (kk0 + (uint64_t)((j * 16) >> NB) < a.nblk) *reinterpret_cast<uint4*>(out_msg + kk0 * B + 16 * (uint64_t)j) = v;
+#pragma unroll
+    for (int h = 0; h < Cf::PER_LANE; ++h) {
+        const int j = lane + 32 * h;
+        if (j < Cf::CHUNKS && kk0 + (uint64_t)((j * 16) >> NB) < a.nblk)
+            *reinterpret_cast<uint4*>(out_msg + kk0 * B + 16 * (uint64_t)j) =
+                *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
     }
     if (live && q == 0) {
         *reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8) = make_float2(alpha, s);
