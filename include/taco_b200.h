@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TACO_B200_ABI_VERSION 2
+#define TACO_B200_ABI_VERSION 3
 
 typedef enum {
     TACO_OK = 0,
@@ -53,6 +53,7 @@ typedef enum { TACO_DT_F32 = 0, TACO_DT_BF16 = 1 } taco_dtype;
 /* d_flags bits */
 #define TACO_FLAG_NONFINITE_INPUT 1 /* -> Input,   "input tensor contains NaN or Inf"         */
 #define TACO_FLAG_BAD_SCALARS 2     /* -> Corrupt, "block scalars must be finite and nonzero" */
+#define TACO_FLAG_PEER_TIMEOUT 4    /* -> Cuda,    "peer barrier timed out" (no counterpart)  */
 
 /* taco::CodecConfig (codec.hpp:24-33).
  * kind (codec.hpp:11-17): 0 = Taco (the fused sm_100a hot path), 1 = DirectFp8,
@@ -148,6 +149,54 @@ int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype
  * the Taco (q_top = q_max) or AshInt8 (q_top = 127) rotation, ceil(n/B)*B fp32 values. */
 int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
                              float* out, int* d_flags, void* stream);
+
+/* ------------------------------------ peer-memory two-shot (SURVEY §8e, B200 extras) -----
+ * The two-shot of collective.cpp:75-111 with the exchange folded into the kernels, no
+ * NCCL call on the data path: K1 stores shard p's message straight into rank p's
+ * receive slot, K3 stores its re-encoded shard into every rank's gather slot (NVLink
+ * stores into CUDA-IPC mapped peer memory, then a system-scope fence), and a device
+ * barrier (system-scope release/acquire flags) separates the phases.  Each rank owns
+ * one region from taco_peer_alloc; the others map it with taco_peer_open on the
+ * exported handle.  taco_peers.base[q] = rank q's region as mapped in this process. */
+#define TACO_MAX_PEERS 8
+typedef struct {
+    unsigned char bytes[64]; /* cudaIpcMemHandle_t */
+} taco_ipc_handle;
+typedef struct {
+    uint32_t nranks, rank;
+    void* base[TACO_MAX_PEERS];
+} taco_peers;
+
+/* device memory on `device` (zeroed, synchronously) that peers can map; *handle exports it */
+int taco_peer_alloc(int device, uint64_t bytes, void** ptr, taco_ipc_handle* handle);
+/* map a peer's exported region into this process (on `device`, this rank's GPU) */
+int taco_peer_open(int device, const taco_ipc_handle* handle, void** ptr);
+int taco_peer_close(void* ptr);
+int taco_peer_free(void* ptr);
+/* bytes of the barrier state at flags_offset: P arrival slots + this rank's epoch */
+uint64_t taco_peer_flags_bytes(void);
+
+/* Device barrier over the ranks of `peers`.  Bumps this rank's epoch (a counter in its
+ * own region, so CUDA-graph replays keep counting), stores it into slot `rank` of every
+ * rank's flag array (base[q] + flags_offset) with release semantics at system scope,
+ * then waits until every slot of its own array has reached it.  Gives up after
+ * timeout_ms, setting TACO_FLAG_PEER_TIMEOUT in d_flags (a dead peer never hangs). */
+int taco_peer_barrier_dev(const taco_peers* peers, uint64_t flags_offset, uint32_t timeout_ms, int* d_flags,
+                          void* stream);
+
+/* K1 into the peers: shard p's message (layout of blk_end - blk_begin blocks) goes to
+ * base[p] + dst_offset + rank*slot_stride.  Taco kind, B <= 1024. */
+int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                           uint64_t blk_begin, uint64_t blk_end, uint64_t dst_offset, uint64_t slot_stride,
+                           int* d_flags, void* stream);
+
+/* K3 into the peers: reduce the P local messages (rank r at msgs + r*rank_stride) and
+ * store the re-encoded shard to base[q] + dst_offset + rank*slot_stride of EVERY rank q
+ * (the phase-2 all-gather done by K3's stores).  acc_out as in taco_reduce_encode_dev. */
+int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride,
+                                const taco_peers* peers, uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end,
+                                uint64_t dst_offset, uint64_t slot_stride, void* acc_out, int acc_dtype,
+                                int* d_flags, void* stream);
 
 /* ------------------------------------------------- TACOCMP1 archive -----
  * serialize.cpp:109-177: "TACOCMP1", kind u8, format id u8, block size u32, length u64,

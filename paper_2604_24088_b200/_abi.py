@@ -21,7 +21,8 @@ E4M3, E5M2 = 0, 1
 # taco::CodecKind (codec.hpp:11-17) and DirectScaleScope (codec.hpp:22)
 TACO, DIRECT_FP8, INT8_UNIFORM, IDENTITY, ASH_INT8 = range(5)
 GLOBAL_MAX, UNIT, PER_BLOCK_MAX = range(3)
-FLAG_NONFINITE_INPUT, FLAG_BAD_SCALARS = 1, 2
+FLAG_NONFINITE_INPUT, FLAG_BAD_SCALARS, FLAG_PEER_TIMEOUT = 1, 2, 4
+MAX_PEERS = 8
 
 # taco::ErrorCode names (proj/include/taco/error.hpp:10-16)
 ERROR_NAMES = {ERR_USAGE: "usage", ERR_CONFIG: "config", ERR_INPUT: "input", ERR_IO: "io",
@@ -63,6 +64,18 @@ class Layout(C.Structure):
                 ("msg_bytes", C.c_uint64), ("msg_stride", C.c_uint64)]
 
 
+class IpcHandle(C.Structure):
+    """taco_ipc_handle (cudaIpcMemHandle_t bytes, exchanged between ranks)."""
+
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
+class Peers(C.Structure):
+    """taco_peers: rank q's peer region as mapped in this process, q < nranks."""
+
+    _fields_ = [("nranks", C.c_uint32), ("rank", C.c_uint32), ("base", C.c_void_p * MAX_PEERS)]
+
+
 def make_config(block_size=256, fmt=E4M3, target_energy=1.0, stability_epsilon=1e-12, kind=TACO,
                 direct_scale=GLOBAL_MAX) -> Config:
     return Config(int(block_size), float(target_energy), float(stability_epsilon), int(fmt), int(kind),
@@ -99,6 +112,16 @@ _SIGNATURES = {
     "taco_archive_import_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P, _P]),
     "taco_scaled_spectrum_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P]),
     "taco_error_report_dev": (C.c_int, [_P, _I, _P, _I, _U64, _U32, C.POINTER(ErrorReportC), _P, _P]),
+    "taco_peer_alloc": (C.c_int, [_I, _U64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
+    "taco_peer_open": (C.c_int, [_I, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),
+    "taco_peer_close": (C.c_int, [_P]),
+    "taco_peer_free": (C.c_int, [_P]),
+    "taco_peer_flags_bytes": (_U64, []),
+    "taco_peer_barrier_dev": (C.c_int, [C.POINTER(Peers), _U64, _U32, _P, _P]),
+    "taco_compress_push_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, C.POINTER(Peers), _U64, _U64, _U64,
+                                         _U64, _P, _P]),
+    "taco_reduce_encode_push_dev": (C.c_int, [C.POINTER(Config), _P, _U64, C.POINTER(Peers), _U64, _U64, _U64,
+                                              _U64, _U64, _P, _I, _P, _P]),
     "taco_fp8_encode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
     "taco_fp8_decode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
 }

@@ -29,6 +29,51 @@ def _timed(fn, steps, stream):
     return float(ms.item())
 
 
+def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
+    """Peer-memory two-shot (K1/K3 store into CUDA-IPC mapped peer regions, device
+    barriers): time it like the NCCL leg and check it against the NCCL leg's result."""
+    from . import collective, peer
+    from ._abi import TacoError
+
+    world = dist.get_world_size()
+    try:
+        par = peer.PeerTwoShotAllReduce(n, cfg, dtype=torch.bfloat16, device=xs[0].device, timeout_ms=20_000)
+    except TacoError as e:
+        return {"error": str(e)}
+    pouts = [torch.empty_like(o) for o in outs]
+    try:
+        graphs = [collective.Graphed(par, xs[i], pouts[i]) for i in range(R)] if not args.eager else None
+
+        def pstep(i):
+            if graphs is not None:
+                graphs[i % R]()
+            else:
+                par(xs[i % R], pouts[i % R])
+
+        for i in range(args.warmup):
+            pstep(i)
+        torch.cuda.synchronize()
+        par.check()
+        ms = _timed(pstep, args.steps, stream) / args.steps
+        par.check()
+        # bit-identical to the NCCL two-shot on the same input, on every rank
+        ar(xs[0], outs[0])
+        par(xs[0], pouts[0])
+        torch.cuda.synchronize()
+        par.check()
+        same = torch.tensor([1 if torch.equal(outs[0].view(torch.int16), pouts[0].view(torch.int16)) else 0],
+                            device=xs[0].device)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        rep = {"ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
+               "speedup_vs_nccl_twoshot": round(step_ms / ms, 3),
+               "bit_identical_to_nccl_twoshot": bool(same.item() == 1),
+               "gpu_launches_per_step": 5, "barriers_per_step": 2}
+    except TacoError as e:
+        rep = {"error": str(e)}
+    par.close()
+    return rep
+
+
 def run_collective(args, rows, cols, clock_sampler, peaks):
     from . import _abi, collective
     from ._abi import make_config
@@ -91,6 +136,10 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
         nccl_step(i)
     nccl_ms = _timed(nccl_step, args.steps, stream) / args.steps
 
+    # the same all-reduce with the exchange done by the kernels' own stores into the peers'
+    # memory (peer.py): no NCCL call on the data path; must be bit-identical to the above
+    peer_rep = _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R)
+
     # e2e: pinned host tensor -> H2D -> compressed all-reduce -> D2H, every step
     xh = xs[0].cpu().pin_memory()
     yh = torch.empty(n, dtype=torch.bfloat16).pin_memory()
@@ -151,6 +200,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
             "e2e": {"value": round(world * 2 * n / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n,
                     "api": "collective.TwoShotAllReduce (pinned host in / out)"},
+            "peer_memory_twoshot": peer_rep,
             "ranks_agree": bool(abs(float(mx.item()) - float(mn.item())) == 0.0),
             "gpu_launches": 3 * len(ar.ch.ranges) * args.steps,
             "clocks": clk.summary(),

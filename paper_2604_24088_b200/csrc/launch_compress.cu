@@ -67,13 +67,13 @@ template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
     if constexpr (FMT == 0 && B == 256 && std::is_same<T, __nv_bfloat16>::value) {
-        if (kernel_family() == 5) {
+        if (kernel_family() == 5 && a.ndst == 0) {
             const cudaError_t e = run_tc(l, a, c);
             if (e != cudaErrorNotSupported) return e;
         }
     }
     if constexpr (FMT == 0 && B >= 32 && B <= 1024) {
-        if (kernel_family() == 3) {
+        if (kernel_family() == 3 && a.ndst == 0) {
             using Cf = r2::Cfg<B, T>;
             const uint64_t tps = (a.nblk + Cf::G - 1) / Cf::G;
             auto* kern = &r2::k_compress_r2<B, T>;
@@ -104,7 +104,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         constexpr int VMAX = 8, EMAX = FMT == 0 ? TACO_K1_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
         using Cf = K1Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
-        auto* kern = &k_compress<B, T, FMT, EMAX, VMAX>;
+        auto* kern = a.ndst ? &k_compress<B, T, FMT, EMAX, VMAX, true> : &k_compress<B, T, FMT, EMAX, VMAX, false>;
         const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
         kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
     } else {

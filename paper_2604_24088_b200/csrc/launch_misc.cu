@@ -221,3 +221,58 @@ int error_report_dev(const void* x, int dx, const void* y, int dy, uint64_t n, u
 }
 
 }  // namespace taco_impl
+
+// ------------------------------------------------------ peer-memory barrier ---
+// One CTA; thread q < P signals rank q and then waits for rank q's signal.  The epoch lives
+// in this rank's own region so a captured CUDA graph keeps counting across replays.
+namespace taco_impl {
+namespace {
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_peer_barrier(PeerSlots f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags) {
+    __shared__ uint32_t e;
+    if (threadIdx.x == 0) {
+        e = *f.epoch + 1;
+        *f.epoch = e;
+    }
+    __syncthreads();
+    const uint32_t q = threadIdx.x;
+    if (q >= P) return;
+    // the peer stores of the kernels before this one on the stream (K1 / K3 pushes) are
+    // complete at this kernel's start (stream order); the system-scope fence + release
+    // store publish them to the peer that acquires the signal
+    __threadfence_system();
+    st_release_sys(f.slot[q] + rank, e);
+    const uint32_t* mine = f.slot[rank] + q;
+    const uint64_t t0 = globaltimer();
+    while ((int32_t)(ld_acquire_sys(mine) - e) < 0) {
+        if (globaltimer() - t0 > timeout_ns) {
+            taco_dev::raise_flag(flags, 4);  // TACO_FLAG_PEER_TIMEOUT
+            break;
+        }
+        __nanosleep(64);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags,
+                                cudaStream_t stream) {
+    k_peer_barrier<<<1, 32, 0, stream>>>(f, rank, P, timeout_ns, flags);
+    return cudaGetLastError();
+}
+
+}  // namespace taco_impl

@@ -208,6 +208,7 @@ uint64_t taco_archive_size(const taco_config* cfg, uint64_t n) {
 int taco_flags_status(int flags) {
     if (flags & TACO_FLAG_NONFINITE_INPUT) return fail(TACO_ERR_INPUT, "input tensor contains NaN or Inf");
     if (flags & TACO_FLAG_BAD_SCALARS) return fail(TACO_ERR_CORRUPT, "block scalars must be finite and nonzero");
+    if (flags & TACO_FLAG_PEER_TIMEOUT) return fail(TACO_ERR_CUDA, "peer barrier timed out");
     return TACO_OK;
 }
 
@@ -284,6 +285,135 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     taco_dev::with_full_blocks(a, b);
     a.full_last = a.full_mid;  // every rank's message covers the same (single) shard
     Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, out_msg, acc_out, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
+        return cuda_fail(e, "K3 reduce-encode launch");
+    return TACO_OK;
+}
+
+// ------------------------------------------------------------ peer-memory two-shot ---
+
+int taco_peer_alloc(int device, uint64_t bytes, void** ptr, taco_ipc_handle* handle) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(taco_ipc_handle), "IPC handle size");
+    if (!ptr || !handle || bytes == 0) return fail(TACO_ERR_USAGE, "peer allocation needs a size and outputs");
+    TACO_CUDA(cudaSetDevice(device));
+    void* p = nullptr;
+    TACO_CUDA(cudaMalloc(&p, bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaMemset(p, 0, bytes);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = cudaIpcGetMemHandle(&h, p);
+    if (e != cudaSuccess) {
+        cudaFree(p);
+        return cuda_fail(e, "peer allocation");
+    }
+    std::memcpy(handle->bytes, &h, sizeof(h));
+    *ptr = p;
+    return TACO_OK;
+}
+
+int taco_peer_open(int device, const taco_ipc_handle* handle, void** ptr) {
+    if (!ptr || !handle) return fail(TACO_ERR_USAGE, "peer open needs a handle");
+    TACO_CUDA(cudaSetDevice(device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle->bytes, sizeof(h));
+    TACO_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return TACO_OK;
+}
+
+int taco_peer_close(void* ptr) {
+    TACO_CUDA(cudaIpcCloseMemHandle(ptr));
+    return TACO_OK;
+}
+
+int taco_peer_free(void* ptr) {
+    TACO_CUDA(cudaFree(ptr));
+    return TACO_OK;
+}
+
+uint64_t taco_peer_flags_bytes(void) { return 4ull * TACO_MAX_PEERS + 16; }
+
+namespace {
+int check_peers(const taco_peers* peers) {
+    if (!peers) return fail(TACO_ERR_USAGE, "null peer set");
+    if (peers->nranks == 0 || peers->nranks > TACO_MAX_PEERS)
+        return fail(TACO_ERR_USAGE, "peer collectives support 1 to 8 ranks");
+    if (peers->rank >= peers->nranks) return fail(TACO_ERR_USAGE, "rank outside the peer set");
+    for (uint32_t q = 0; q < peers->nranks; ++q)
+        if (!peers->base[q]) return fail(TACO_ERR_USAGE, "peer region not mapped");
+    return TACO_OK;
+}
+
+int check_push_cfg(const taco_config* cfg) {
+    if (int rc = check_config(cfg)) return rc;
+    if (cfg->kind != 0) return fail(TACO_ERR_USAGE, "peer collectives serve CodecKind::Taco");
+    if (cfg->block_size > 1024) return fail(TACO_ERR_USAGE, "peer collectives support block sizes up to 1024");
+    return TACO_OK;
+}
+}  // namespace
+
+int taco_peer_barrier_dev(const taco_peers* peers, uint64_t flags_offset, uint32_t timeout_ms, int* d_flags,
+                          void* stream) {
+    if (int rc = check_peers(peers)) return rc;
+    if (flags_offset % 16) return fail(TACO_ERR_USAGE, "peer flag offset must be 16-byte aligned");
+    taco_impl::PeerSlots f{};
+    for (uint32_t q = 0; q < peers->nranks; ++q)
+        f.slot[q] = reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(peers->base[q]) + flags_offset);
+    f.epoch = f.slot[peers->rank] + TACO_MAX_PEERS;
+    if (cudaError_t e = taco_impl::launch_peer_barrier(f, peers->rank, peers->nranks,
+                                                       (uint64_t)timeout_ms * 1000000ull, d_flags,
+                                                       (cudaStream_t)stream))
+        return cuda_fail(e, "peer barrier launch");
+    return TACO_OK;
+}
+
+int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                           uint64_t blk_begin, uint64_t blk_end, uint64_t dst_offset, uint64_t slot_stride,
+                           int* d_flags, void* stream) {
+    if (int rc = check_push_cfg(cfg)) return rc;
+    if (int rc = check_peers(peers)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint32_t P = peers->nranks;
+    const uint64_t b = cfg->block_size, S = div_up(n, P), m = div_up(S, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    ShardArgs a{n, S, P, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset,
+                aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a, b);
+    for (uint32_t q = 0; q < P; ++q)
+        a.dst[q] = static_cast<uint8_t*>(peers->base[q]) + dst_offset + (uint64_t)peers->rank * slot_stride;
+    a.ndst = P;
+    Launch l{cfg->block_size, dtype, (int)cfg->format, x, a.dst[0], nullptr, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_compress(l, a, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    return TACO_OK;
+}
+
+int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride,
+                                const taco_peers* peers, uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end,
+                                uint64_t dst_offset, uint64_t slot_stride, void* acc_out, int acc_dtype,
+                                int* d_flags, void* stream) {
+    if (int rc = check_push_cfg(cfg)) return rc;
+    if (int rc = check_peers(peers)) return rc;
+    if (acc_out)
+        if (int rc = check_dtype(acc_dtype)) return rc;
+    if (shard_len == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint32_t P = peers->nranks;
+    const uint64_t b = cfg->block_size, m = div_up(shard_len, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (P > 1 && rank_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    ShardArgs a{shard_len, shard_len, P, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
+                acc_out ? aligned16(acc_out) : 0, d_flags};
+    taco_dev::with_full_blocks(a, b);
+    a.full_last = a.full_mid;
+    for (uint32_t q = 0; q < P; ++q)
+        a.dst[q] = static_cast<uint8_t*>(peers->base[q]) + dst_offset + (uint64_t)peers->rank * slot_stride;
+    a.ndst = P;
+    Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, a.dst[0], acc_out, (cudaStream_t)stream};
     if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
         return cuda_fail(e, "K3 reduce-encode launch");
     return TACO_OK;

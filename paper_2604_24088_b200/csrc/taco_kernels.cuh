@@ -18,6 +18,8 @@
 
 namespace taco_dev {
 
+constexpr int kMaxPeers = 8;  // peer-memory collectives: ranks of one NVLink domain (TP <= 8)
+
 struct ShardArgs {
     uint64_t n;           // logical elements of the tensor (K1/K2)
     uint64_t S;           // shard length
@@ -31,7 +33,19 @@ struct ShardArgs {
     // leading blocks of the chunk that are whole (no shard / tensor tail) in a shard other
     // than the last and in the last one (host-computed by with_full_blocks)
     uint64_t full_mid = 0, full_last = 0;
+    // peer-memory collectives (ndst > 0): K1 writes shard p's message to dst[p] and K3
+    // writes its re-encoded shard to every dst[0..ndst) -- stores straight into the
+    // peers' receive buffers over NVLink.  Their visibility to the peers is established
+    // by the next kernel on the stream, the peer barrier (fence.sc.sys, then a
+    // st.release.sys signal), not by per-thread fences (one per warp of a 5,120-CTA K3
+    // cost 2.3x its run time)
+    uint8_t* dst[kMaxPeers] = {};
+    uint32_t ndst = 0;
 };
+
+__device__ __forceinline__ uint8_t* shard_msg(uint8_t* msgs, const ShardArgs& a, uint64_t p) {
+    return a.ndst ? a.dst[p] : msgs + p * a.msg_stride;
+}
 
 // number of whole blocks of a chunk; every kernel's "is this tile full" is one compare
 __host__ __device__ inline void with_full_blocks(ShardArgs& a, uint64_t B) {
@@ -150,7 +164,9 @@ struct K1Cfg {
 };
 
 // --------------------------------------------------------------------------- K1 ---
-template <int B, typename TIn, int FMT, int EMAX, int VMAX>
+// PUSH: peer-memory mode (ShardArgs::dst), a separate instantiation so the default
+// kernel keeps its register allocation
+template <int B, typename TIn, int FMT, int EMAX, int VMAX, bool PUSH = false>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
                                                               ShardArgs a, CodecConsts c, FastDiv tps) {
     using Cf = K1Cfg<B, TIn, FMT, EMAX, VMAX>;
@@ -217,7 +233,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
         double ss;
         quantise<L>(v, q, c, alpha, s, ss);
         if (live) {
-            uint8_t* m = msgs + p * a.msg_stride;
+            uint8_t* m = PUSH ? a.dst[p] : msgs + p * a.msg_stride;
 #pragma unroll
             for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
             if (q == 0) {
@@ -386,12 +402,14 @@ __global__ void __launch_bounds__(kWarpThreads) k_reduce_encode(const uint8_t* _
     double ss;
     quantise<L>(acc, q, c, alpha, s, ss);
     if (!live) return;
+    const uint32_t nd = a.ndst ? a.ndst : 1;
+    for (uint32_t d = 0; d < nd; ++d) {  // peer mode: the same message into every rank's buffer
+        uint8_t* o = a.ndst ? a.dst[d] : out_msg;
 #pragma unroll
-    for (int j = 0; j < NV; ++j) acc.template store_codes_at<FMT, V>(j, out_msg + kk * B + Gm::pos(j, q));
-    if (q == 0) {
-        *reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8) = make_float2(alpha, s);
-        if (bad) raise_flag(a.flags, 2);
+        for (int j = 0; j < NV; ++j) acc.template store_codes_at<FMT, V>(j, o + kk * B + Gm::pos(j, q));
+        if (q == 0) *reinterpret_cast<float2*>(o + a.scal_off + kk * 8) = make_float2(alpha, s);
     }
+    if (q == 0 && bad) raise_flag(a.flags, 2);
 }
 
 // ===================================================== big blocks (B >= 2048) ===

@@ -65,6 +65,15 @@ int error_report_dev(const void* x, int dx, const void* y, int dy, uint64_t n, u
 cudaError_t launch_archive(const uint8_t* src, uint8_t* dst, uint64_t nblocks, uint64_t payload, uint64_t scal_off,
                            const uint8_t* hdr22, int mode, int* flags, cudaStream_t stream);
 
+// peer-memory barrier: slot[q] = rank q's arrival array (kMaxPeers u32) as mapped here,
+// epoch = this rank's barrier counter
+struct PeerSlots {
+    uint32_t* slot[taco_dev::kMaxPeers];
+    uint32_t* epoch;
+};
+cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags,
+                                cudaStream_t stream);
+
 inline taco_dev::FastDiv make_fastdiv(uint32_t d) {
     uint32_t s = 0;
     while ((1ull << s) < d) ++s;

@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         uint8_t* cb = reinterpret_cast<uint8_t*>(xb);
         stage_codes<NB>(cb, w, g, q);
         __syncwarp();
-        uint8_t* m = msgs + p * a.msg_stride;
+        uint8_t* m = shard_msg(msgs, a, p);
         const uint64_t kk = kk0 + g;
         // coalesced copy-out: chunk j (16 codes) of the tile belongs to block j*16/B
 #pragma unroll
@@ -860,17 +860,24 @@ __global__ void __launch_bounds__(kTileWarps * 32)
     uint8_t* cb = reinterpret_cast<uint8_t*>(xb);
     stage_codes<NB>(cb, acc, g, q);
     __syncwarp();
+    uint4 cv[Cf::PER_LANE];
 #pragma unroll
     for (int h = 0; h < Cf::PER_LANE; ++h) {
         const int j = lane + 32 * h;
-        if (j < Cf::CHUNKS && kk0 + (uint64_t)((j * 16) >> NB) < a.nblk)
-            *reinterpret_cast<uint4*>(out_msg + kk0 * B + 16 * (uint64_t)j) =
-                *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
+        if (j < Cf::CHUNKS) cv[h] = *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
     }
-    if (live && q == 0) {
-        *reinterpret_cast<float2*>(out_msg + a.scal_off + kk * 8) = make_float2(alpha, s);
-        if (!ok) raise_flag(a.flags, 2);
+    const uint32_t nd = a.ndst ? a.ndst : 1;
+    for (uint32_t d = 0; d < nd; ++d) {  // peer mode: the same message into every rank's buffer
+        uint8_t* o = a.ndst ? a.dst[d] : out_msg;
+#pragma unroll
+        for (int h = 0; h < Cf::PER_LANE; ++h) {
+            const int j = lane + 32 * h;
+            if (j < Cf::CHUNKS && kk0 + (uint64_t)((j * 16) >> NB) < a.nblk)
+                *reinterpret_cast<uint4*>(o + kk0 * B + 16 * (uint64_t)j) = cv[h];
+        }
+        if (live && q == 0) *reinterpret_cast<float2*>(o + a.scal_off + kk * 8) = make_float2(alpha, s);
     }
+    if (live && q == 0 && !ok) raise_flag(a.flags, 2);
 }
 
 }  // namespace tile

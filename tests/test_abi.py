@@ -19,7 +19,7 @@ def test_library_exports_every_header_symbol():
     out = subprocess.run(["nm", "-D", "--defined-only", _abi.LIB_PATH], capture_output=True, text=True).stdout
     exported = {line.split()[-1] for line in out.splitlines() if line.strip()}
     assert set(syms) <= exported
-    assert lib.taco_abi_version() == 2
+    assert lib.taco_abi_version() == 3
 
 
 def test_default_config_matches_reference_defaults():
@@ -108,3 +108,29 @@ def test_product_does_not_reference_the_oracle():
     out = subprocess.run(["nm", "-D", _abi.LIB_PATH], capture_output=True, text=True).stdout
     names = {line.split()[-1] for line in out.splitlines() if line.strip()}
     assert not any(s.startswith(("tor_", "ref_")) for s in names)
+
+
+def test_peer_abi_argument_checks_without_a_gpu():
+    """The peer-memory entry points validate their peer set before touching the device."""
+    import ctypes as C
+    lib = _abi.lib()
+    cfg = make_config()
+    assert lib.taco_peer_flags_bytes() >= 4 * _abi.MAX_PEERS + 4
+    cases = []
+    ps = _abi.Peers(); ps.nranks = 9; cases.append((ps, "1 to 8 ranks"))
+    ps = _abi.Peers(); ps.nranks = 0; cases.append((ps, "1 to 8 ranks"))
+    ps = _abi.Peers(); ps.nranks, ps.rank = 2, 2; cases.append((ps, "rank outside the peer set"))
+    ps = _abi.Peers(); ps.nranks, ps.rank = 2, 0; ps.base[0] = 4096; cases.append((ps, "peer region not mapped"))
+    for ps, msg in cases:
+        for rc in (lib.taco_compress_push_dev(C.byref(cfg), None, 1, 100, C.byref(ps), 0, 1, 0, 0, None, None),
+                   lib.taco_reduce_encode_push_dev(C.byref(cfg), None, 0, C.byref(ps), 100, 0, 1, 0, 0, None, 0,
+                                                   None, None),
+                   lib.taco_peer_barrier_dev(C.byref(ps), 0, 10, None, None)):
+            assert rc == _abi.ERR_USAGE and msg in lib.taco_last_error().decode()
+    ps = _abi.Peers(); ps.nranks, ps.rank = 1, 0; ps.base[0] = 4096
+    assert lib.taco_compress_push_dev(C.byref(make_config(4096)), None, 1, 100, C.byref(ps), 0, 1, 0, 0, None,
+                                      None) == _abi.ERR_USAGE
+    assert "up to 1024" in lib.taco_last_error().decode()
+    assert lib.taco_peer_barrier_dev(C.byref(ps), 8, 10, None, None) == _abi.ERR_USAGE
+    assert lib.taco_flags_status(_abi.FLAG_PEER_TIMEOUT) == _abi.ERR_CUDA
+    assert lib.taco_last_error().decode() == "peer barrier timed out"
