@@ -190,6 +190,13 @@ int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uin
                            uint64_t blk_begin, uint64_t blk_end, uint64_t dst_offset, uint64_t slot_stride,
                            int* d_flags, void* stream);
 
+/* K1 broadcast (the SP all-gather): ONE message of this rank's n-element tensor (layout of
+ * blk_end - blk_begin blocks) stored to base[q] + dst_offset + rank*slot_stride of EVERY
+ * rank q.  Taco kind, B <= 1024. */
+int taco_compress_bcast_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                            uint64_t blk_begin, uint64_t blk_end, uint64_t dst_offset, uint64_t slot_stride,
+                            int* d_flags, void* stream);
+
 /* K3 into the peers: reduce the P local messages (rank r at msgs + r*rank_stride) and
  * store the re-encoded shard to base[q] + dst_offset + rank*slot_stride of EVERY rank q
  * (the phase-2 all-gather done by K3's stores).  acc_out as in taco_reduce_encode_dev. */

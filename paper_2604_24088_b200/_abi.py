@@ -120,6 +120,8 @@ _SIGNATURES = {
     "taco_peer_barrier_dev": (C.c_int, [C.POINTER(Peers), _U64, _U32, _P, _P]),
     "taco_compress_push_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, C.POINTER(Peers), _U64, _U64, _U64,
                                          _U64, _P, _P]),
+    "taco_compress_bcast_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, C.POINTER(Peers), _U64, _U64, _U64,
+                                          _U64, _P, _P]),
     "taco_reduce_encode_push_dev": (C.c_int, [C.POINTER(Config), _P, _U64, C.POINTER(Peers), _U64, _U64, _U64,
                                               _U64, _U64, _P, _I, _P, _P]),
     "taco_fp8_encode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),

@@ -390,6 +390,29 @@ int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uin
     return TACO_OK;
 }
 
+int taco_compress_bcast_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                            uint64_t blk_begin, uint64_t blk_end, uint64_t dst_offset, uint64_t slot_stride,
+                            int* d_flags, void* stream) {
+    if (int rc = check_push_cfg(cfg)) return rc;
+    if (int rc = check_peers(peers)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint64_t b = cfg->block_size, m = div_up(n, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    if (peers->nranks > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    ShardArgs a{n, n, 1, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset, aligned16(x), d_flags};
+    taco_dev::with_full_blocks(a, b);
+    for (uint32_t q = 0; q < peers->nranks; ++q)
+        a.dst[q] = static_cast<uint8_t*>(peers->base[q]) + dst_offset + (uint64_t)peers->rank * slot_stride;
+    a.ndst = peers->nranks;
+    a.bcast = 1;
+    Launch l{cfg->block_size, dtype, (int)cfg->format, x, a.dst[0], nullptr, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_compress(l, a, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    return TACO_OK;
+}
+
 int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64_t rank_stride,
                                 const taco_peers* peers, uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end,
                                 uint64_t dst_offset, uint64_t slot_stride, void* acc_out, int acc_dtype,

@@ -41,6 +41,7 @@ struct ShardArgs {
     // cost 2.3x its run time)
     uint8_t* dst[kMaxPeers] = {};
     uint32_t ndst = 0;
+    uint32_t bcast = 0;  // K1 with ndst > 0: shard 0's message to every dst (all-gather)
 };
 
 __device__ __forceinline__ uint8_t* shard_msg(uint8_t* msgs, const ShardArgs& a, uint64_t p) {
@@ -233,13 +234,20 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
         double ss;
         quantise<L>(v, q, c, alpha, s, ss);
         if (live) {
-            uint8_t* m = PUSH ? a.dst[p] : msgs + p * a.msg_stride;
+            auto put = [&](uint8_t* m) {
 #pragma unroll
-            for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
-            if (q == 0) {
-                *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
-                if (!isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
+                for (int j = 0; j < NV; ++j) v.template store_codes_at<FMT, V>(j, m + kk * B + Gm::pos(j, q));
+                if (q == 0) *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
+            };
+            if constexpr (PUSH) {
+                if (a.bcast)
+                    for (uint32_t d = 0; d < a.ndst; ++d) put(a.dst[d]);
+                else
+                    put(a.dst[p]);
+            } else {
+                put(msgs + p * a.msg_stride);
             }
+            if (q == 0 && !isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
         }
     }
 }

@@ -481,19 +481,21 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         uint8_t* cb = reinterpret_cast<uint8_t*>(xb);
         stage_codes<NB>(cb, w, g, q);
         __syncwarp();
-        uint8_t* m = shard_msg(msgs, a, p);
         const uint64_t kk = kk0 + g;
         // coalesced copy-out: chunk j (16 codes) of the tile belongs to block j*16/B
+        // (peer all-gather: the same message to every rank)
+        const uint32_t nd = a.bcast ? a.ndst : 1;
+        for (uint32_t d = 0; d < nd; ++d) {
+            uint8_t* m = a.bcast ? a.dst[d] : shard_msg(msgs, a, p);
 #pragma unroll
-        for (int j = lane; j < Gm::TILE / 16; j += 32) {
-            const uint4 v = *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
-            if (full || kk0 + (uint64_t)((j * 16) >> NB) < a.nblk)
-                *reinterpret_cast<uint4*>(m + kk0 * B + 16 * (uint64_t)j) = v;
+            for (int j = lane; j < Gm::TILE / 16; j += 32) {
+                const uint4 v = *reinterpret_cast<const uint4*>(cb + 16 * swz((uint32_t)j));
+                if (full || kk0 + (uint64_t)((j * 16) >> NB) < a.nblk)
+                    *reinterpret_cast<uint4*>(m + kk0 * B + 16 * (uint64_t)j) = v;
+            }
+            if (q == 0 && kk < a.nblk) *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
         }
-        if (q == 0 && kk < a.nblk) {
-            *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
-            if (!isfinite(ss)) raise_flag(a.flags, 1);
-        }
+        if (q == 0 && kk < a.nblk && !isfinite(ss)) raise_flag(a.flags, 1);
         slot = slot + 1 == D ? 0 : slot + 1;
     }
 }

@@ -113,31 +113,20 @@ def decode(cfg: Config, peers: Peers, geo: PeerLayout, n: int, out: torch.Tensor
                                               flags.ptr(), C.c_void_p(_stream(stream))))
 
 
-class PeerTwoShotAllReduce:
-    """FP8 two-shot all-reduce of a fixed-size tensor over peer memory (one process per GPU).
+class _Mapped:
+    """This rank's region, every peer's region mapped here, and the taco_peers view."""
 
-    Same contract as collective.TwoShotAllReduce (bit-identical results); the group is
-    only used once, to exchange the IPC handles of the regions."""
-
-    def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
-                 device=None, timeout_ms: int = 10_000):
+    def __init__(self, nbytes: int, group, device: torch.device):
         self.group = group
         self.P = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
         if self.P > _abi.MAX_PEERS:
             raise TacoError(_abi.ERR_USAGE, "peer collectives support 1 to 8 ranks")
-        self.cfg = cfg if cfg is not None else _abi.make_config()
-        self.n, self.dtype = n, dtype
-        self.out_dtype = out_dtype or dtype
-        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.timeout_ms = timeout_ms
-        self.geo = PeerLayout(self.cfg, n, self.P)
-        self.flags = Flags(self.device)
-        dix = self.device.index if self.device.index is not None else torch.cuda.current_device()
-        self.region = PeerRegion(self.geo.nbytes, dix)
+        dix = device.index if device.index is not None else torch.cuda.current_device()
+        self.region = PeerRegion(nbytes, dix)
         handles = [None] * self.P
         dist.all_gather_object(handles, self.region.handle_bytes(), group=group)
-        self.bases, self._opened = [], []
+        self.bases, self.opened = [], []
         err = ""
         try:
             for q in range(self.P):
@@ -145,7 +134,7 @@ class PeerTwoShotAllReduce:
                     self.bases.append(self.region.ptr)
                 else:
                     p = open_handle(handles[q], dix)
-                    self._opened.append(p)
+                    self.opened.append(p)
                     self.bases.append(p)
         except TacoError as e:  # e.g. no P2P path between two GPUs
             err = f"rank {self.rank}: {e}"
@@ -155,12 +144,51 @@ class PeerTwoShotAllReduce:
         dist.all_gather_object(errs, err, group=group)
         bad = [e for e in errs if e]
         if bad:
-            for p in self._opened:
-                _abi.lib().taco_peer_close(p)
-            self._opened = []
+            self._unmap()
             self.region.free()
             raise TacoError(_abi.ERR_CUDA, "peer mapping failed: " + "; ".join(bad))
         self.peers = peers_struct(self.bases, self.rank)
+
+    @property
+    def own(self) -> int:
+        return self.peers.base[self.rank]
+
+    def _unmap(self):
+        for p in self.opened:
+            _abi.lib().taco_peer_close(p)
+        self.opened = []
+
+    def close(self, device):
+        """Collective: unmap the peers' regions, then free this rank's own."""
+        torch.cuda.synchronize(device)
+        dist.barrier(group=self.group)
+        self._unmap()
+        dist.barrier(group=self.group)
+        self.region.free()
+
+
+def _device(device):
+    return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+
+
+class PeerTwoShotAllReduce:
+    """FP8 two-shot all-reduce of a fixed-size tensor over peer memory (one process per GPU).
+
+    Same contract as collective.TwoShotAllReduce (bit-identical results); the group is
+    only used once, to exchange the IPC handles of the regions."""
+
+    def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 device=None, timeout_ms: int = 10_000):
+        self.cfg = cfg if cfg is not None else _abi.make_config()
+        self.n, self.dtype = n, dtype
+        self.out_dtype = out_dtype or dtype
+        self.device = _device(device)
+        self.timeout_ms = timeout_ms
+        self.P = dist.get_world_size(group)
+        self.geo = PeerLayout(self.cfg, n, self.P)
+        self.flags = Flags(self.device)
+        self.map = _Mapped(self.geo.nbytes, group, self.device)
+        self.peers = self.map.peers
 
     @property
     def shard_len(self) -> int:
@@ -182,14 +210,102 @@ class PeerTwoShotAllReduce:
         self.flags.check()
 
     def close(self):
-        """Collective: unmap the peers' regions, then free this rank's own."""
-        torch.cuda.synchronize(self.device)
-        dist.barrier(group=self.group)
-        for p in self._opened:
-            _abi.check(_abi.lib().taco_peer_close(p))
-        self._opened = []
-        dist.barrier(group=self.group)
-        self.region.free()
+        self.map.close(self.device)
+
+
+class PeerReduceScatter:
+    """Sequence-parallel reduce-scatter over peer memory: K1 pushes shard p into rank p's
+    receive slot, barrier, K3 writes the ascending-rank fp32 sum of this rank's shard
+    (no re-encode), barrier (the receive slots are free again).  Bit-identical to
+    collective.CompressedReduceScatter."""
+
+    def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 device=None, timeout_ms: int = 10_000):
+        self.cfg = cfg if cfg is not None else _abi.make_config()
+        self.n, self.dtype = n, dtype
+        self.out_dtype = out_dtype or dtype
+        self.device = _device(device)
+        self.timeout_ms = timeout_ms
+        self.P = dist.get_world_size(group)
+        self.geo = PeerLayout(self.cfg, n, self.P)
+        self.flags = Flags(self.device)
+        self.map = _Mapped(self.geo.nbytes, group, self.device)
+
+    @property
+    def shard_len(self) -> int:
+        return self.geo.S
+
+    def wire_bytes_per_rank(self) -> int:
+        return (self.P - 1) * self.geo.lay.msg_bytes
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        x = x.reshape(-1)
+        if x.numel() != self.n:
+            raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
+        if out is None:
+            out = torch.empty(self.geo.S, dtype=self.out_dtype, device=self.device)
+        g, ps, lib = self.geo, self.map.peers, _abi.lib()
+        st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
+        _abi.check(lib.taco_compress_push_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n, C.byref(ps),
+                                              0, g.m, g.recv_off, g.stride, fl, st))
+        _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), g.flags_off, self.timeout_ms, fl, st))
+        _abi.check(lib.taco_reduce_encode_dev(C.byref(self.cfg), C.c_void_p(self.map.own + g.recv_off), g.stride,
+                                              self.P, g.S, 0, g.m, None, _ptr(out), _dtype_code(out.dtype), fl, st))
+        _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), g.flags_off, self.timeout_ms, fl, st))
+        return out
+
+    def check(self):
+        self.flags.check()
+
+    def close(self):
+        self.map.close(self.device)
+
+
+class PeerAllGather:
+    """Sequence-parallel all-gather over peer memory: K1 of the own [n_local] slice stored
+    into EVERY rank's gather slot [my rank], barrier, K2 of the P gathered messages,
+    barrier (the gather slots are free again).  Bit-identical to collective.CompressedAllGather."""
+
+    def __init__(self, n_local: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 device=None, timeout_ms: int = 10_000):
+        self.cfg = cfg if cfg is not None else _abi.make_config()
+        self.n_local = n_local
+        self.out_dtype = out_dtype or dtype
+        self.device = _device(device)
+        self.timeout_ms = timeout_ms
+        self.P = dist.get_world_size(group)
+        self.m = cdiv(n_local, self.cfg.block_size)
+        self.lay = _abi.msg_layout(self.cfg, self.m)
+        self.stride = self.lay.msg_stride
+        self.flags_off = _align16(self.P * self.stride)
+        self.flags = Flags(self.device)
+        self.map = _Mapped(self.flags_off + int(_abi.lib().taco_peer_flags_bytes()), group, self.device)
+
+    def wire_bytes_per_rank(self) -> int:
+        return (self.P - 1) * self.lay.msg_bytes
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        x = x.reshape(-1)
+        if x.numel() != self.n_local:
+            raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
+        n = self.P * self.n_local
+        if out is None:
+            out = torch.empty(n, dtype=self.out_dtype, device=self.device)
+        ps, lib = self.map.peers, _abi.lib()
+        st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
+        _abi.check(lib.taco_compress_bcast_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n_local,
+                                               C.byref(ps), 0, self.m, 0, self.stride, fl, st))
+        _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), self.flags_off, self.timeout_ms, fl, st))
+        _abi.check(lib.taco_decompress_dev(C.byref(self.cfg), C.c_void_p(self.map.own), self.stride, self.P, n, 0,
+                                           self.m, _ptr(out), _dtype_code(out.dtype), fl, st))
+        _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), self.flags_off, self.timeout_ms, fl, st))
+        return out
+
+    def check(self):
+        self.flags.check()
+
+    def close(self):
+        self.map.close(self.device)
 
 
 def allreduce_sim_peer(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float32) -> torch.Tensor:
@@ -219,6 +335,65 @@ def allreduce_sim_peer(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float3
                                                        geo.stride, None, _abi.DT_F32, flags.ptr(), st))
         for r in range(P):
             decode(cfg, peers[r], geo, n, outs[r], flags)
+        torch.cuda.synchronize(inputs.device)
+        flags.check()
+        return outs
+    finally:
+        torch.cuda.synchronize(inputs.device)
+        for r in regions:
+            r.free()
+
+
+def reduce_scatter_sim_peer(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float32) -> torch.Tensor:
+    """PeerReduceScatter's kernels for P simulated ranks in one process: [P, S]."""
+    P, n = inputs.shape
+    geo = PeerLayout(cfg, n, P)
+    dix = inputs.device.index if inputs.device.index is not None else torch.cuda.current_device()
+    regions = [PeerRegion(geo.nbytes, dix) for _ in range(P)]
+    try:
+        bases = [r.ptr for r in regions]
+        peers = [peers_struct(bases, r) for r in range(P)]
+        flags = Flags(inputs.device)
+        lib, st = _abi.lib(), C.c_void_p(_stream(None))
+        outs = torch.empty((P, geo.S), dtype=out_dtype, device=inputs.device)
+        for r in range(P):
+            x = inputs[r].contiguous()
+            _abi.check(lib.taco_compress_push_dev(C.byref(cfg), _ptr(x), _dtype_code(x.dtype), n, C.byref(peers[r]),
+                                                  0, geo.m, geo.recv_off, geo.stride, flags.ptr(), st))
+        for r in range(P):
+            _abi.check(lib.taco_reduce_encode_dev(C.byref(cfg), C.c_void_p(peers[r].base[r] + geo.recv_off),
+                                                  geo.stride, P, geo.S, 0, geo.m, None, _ptr(outs[r]),
+                                                  _dtype_code(out_dtype), flags.ptr(), st))
+        torch.cuda.synchronize(inputs.device)
+        flags.check()
+        return outs
+    finally:
+        torch.cuda.synchronize(inputs.device)
+        for r in regions:
+            r.free()
+
+
+def all_gather_sim_peer(inputs: torch.Tensor, cfg: Config, out_dtype=torch.float32) -> torch.Tensor:
+    """PeerAllGather's kernels for P simulated ranks in one process: inputs [P, n_local]
+    -> [P, P * n_local]."""
+    P, nl = inputs.shape
+    m = cdiv(nl, cfg.block_size)
+    stride = _abi.msg_layout(cfg, m).msg_stride
+    dix = inputs.device.index if inputs.device.index is not None else torch.cuda.current_device()
+    regions = [PeerRegion(_align16(P * stride) + int(_abi.lib().taco_peer_flags_bytes()), dix) for _ in range(P)]
+    try:
+        bases = [r.ptr for r in regions]
+        peers = [peers_struct(bases, r) for r in range(P)]
+        flags = Flags(inputs.device)
+        lib, st = _abi.lib(), C.c_void_p(_stream(None))
+        outs = torch.empty((P, P * nl), dtype=out_dtype, device=inputs.device)
+        for r in range(P):
+            x = inputs[r].contiguous()
+            _abi.check(lib.taco_compress_bcast_dev(C.byref(cfg), _ptr(x), _dtype_code(x.dtype), nl,
+                                                   C.byref(peers[r]), 0, m, 0, stride, flags.ptr(), st))
+        for r in range(P):
+            _abi.check(lib.taco_decompress_dev(C.byref(cfg), C.c_void_p(peers[r].base[r]), stride, P, P * nl, 0, m,
+                                               _ptr(outs[r]), _dtype_code(out_dtype), flags.ptr(), st))
         torch.cuda.synchronize(inputs.device)
         flags.check()
         return outs

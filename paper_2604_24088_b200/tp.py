@@ -31,13 +31,18 @@ def _key(kind, group, n, dtype, cfg: Config, chunks):
     return (kind, id(group), n, dtype, cfg.block_size, cfg.format, cfg.kind, chunks)
 
 
-def _get(kind, group, n, dtype, cfg, chunks, device, codec):
-    k = _key(kind, group, n, dtype, cfg, chunks) + (id(codec),)
+def _get(kind, group, n, dtype, cfg, chunks, device, codec, transport="nccl"):
+    k = _key(kind, group, n, dtype, cfg, chunks) + (id(codec), transport)
     op = _CACHE.get(k)
     if op is None:
-        cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
-               "ag": collective.CompressedAllGather}[kind]
-        op = cls(n, cfg, group, dtype=dtype, chunks=chunks, device=device, codec=codec)
+        if transport == "peer":  # exchange inside the kernels (peer.py)
+            from . import peer
+            cls = {"ar": peer.PeerTwoShotAllReduce, "rs": peer.PeerReduceScatter, "ag": peer.PeerAllGather}[kind]
+            op = cls(n, cfg, group, dtype=dtype, device=device)
+        else:
+            cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
+                   "ag": collective.CompressedAllGather}[kind]
+            op = cls(n, cfg, group, dtype=dtype, chunks=chunks, device=device, codec=codec)
         _CACHE[k] = op
     return op
 
@@ -45,18 +50,26 @@ def _get(kind, group, n, dtype, cfg, chunks, device, codec):
 class TpContext:
     """Settings shared by the regions of one model: group, codec config, chunking, codec."""
 
-    def __init__(self, group=None, cfg: Config | None = None, chunks: int = 1, codec=None):
+    def __init__(self, group=None, cfg: Config | None = None, chunks: int = 1, codec=None, transport: str = "nccl"):
+        """transport: "nccl" (K1 -> NCCL all-to-all -> K3 -> NCCL all-gather -> K2, chunked overlap)
+        or "peer" (K1/K3 store into the peers' CUDA-IPC mapped buffers, device barriers;
+        bit-identical results, no NCCL call on the data path)."""
+        if transport not in ("nccl", "peer"):
+            raise ValueError("transport must be 'nccl' or 'peer'")
+        if transport == "peer" and codec is not None:
+            raise ValueError("the peer transport runs the CUDA kernels only")
         self.group = group
         self.cfg = cfg if cfg is not None else _abi.make_config()
         self.chunks = chunks
         self.codec = codec
+        self.transport = transport
 
     @property
     def world(self) -> int:
         return dist.get_world_size(self.group)
 
     def all_reduce(self, x: torch.Tensor) -> torch.Tensor:
-        op = _get("ar", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec)
+        op = _get("ar", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
         return op(x.contiguous()).view(x.shape)
 
     def reduce_scatter(self, x: torch.Tensor) -> torch.Tensor:
@@ -64,12 +77,12 @@ class TpContext:
         w = self.world
         if x.shape[0] % w:
             raise _abi.TacoError(_abi.ERR_USAGE, "sequence length must divide by the tensor-parallel size")
-        op = _get("rs", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec)
+        op = _get("rs", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
         return op(x.contiguous()).view(x.shape[0] // w, *x.shape[1:])
 
     def all_gather(self, x: torch.Tensor) -> torch.Tensor:
         """x: this rank's token slice [t, ...] -> [world * t, ...]"""
-        op = _get("ag", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec)
+        op = _get("ag", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
         return op(x.contiguous()).view(self.world * x.shape[0], *x.shape[1:])
 
 

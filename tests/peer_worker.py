@@ -58,6 +58,26 @@ def main():
         want = codec.allreduce_sim(ins, cfg)
         assert torch.equal(out.view(torch.int32), want.view(torch.int32)), f"rank {rank} graph replay {it}"
     ar.close()
+    # sequence-parallel pair: reduce-scatter (fp32 stage-1 sums) and all-gather
+    S = -(-n // world)
+    rs = peer.PeerReduceScatter(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000)
+    ag = peer.PeerAllGather(S, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000)
+    for it in range(2):
+        ins = inputs_for(world, n, dtype, 3000 + it)
+        stage1 = torch.empty(world * S, dtype=torch.float32, device="cuda")
+        codec.allreduce_sim(ins, cfg, stage1=stage1)
+        got = rs(ins[rank])
+        torch.cuda.synchronize()
+        rs.check()
+        assert torch.equal(got.view(torch.int32), stage1[rank * S:(rank + 1) * S].view(torch.int32)), f"rs {it}"
+        sl = inputs_for(world, S, dtype, 4000 + it)
+        want = torch.cat([codec.decompress(codec.compress(sl[r], cfg), S, cfg) for r in range(world)])
+        got = ag(sl[rank])
+        torch.cuda.synchronize()
+        ag.check()
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), f"ag {it}"
+    rs.close()
+    ag.close()
     dist.destroy_process_group()
     print(f"PEER_OK {rank}", flush=True)
 

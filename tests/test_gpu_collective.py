@@ -145,3 +145,27 @@ def test_tp_regions_and_custom_ops_on_gpu(port, nccl_world1):
     assert torch.equal(msg, codec.compress(local, cfg)[0])
     back = torch.ops.taco_b200.decompress(msg, local.numel(), 256, 0, torch.float32)
     assert torch.equal(back, codec.decompress(codec.compress(local, cfg), local.numel(), cfg))
+
+
+def test_tp_peer_transport_matches_nccl(port, nccl_world1):
+    """TpContext(transport="peer") (kernels store into the peers' mapped buffers) gives the same
+    bits as the NCCL transport for the row-parallel forward / backward and the SP pair."""
+    from paper_2604_24088_b200 import tp
+
+    cfg = make_config(256)
+    T, H, F = 256, 512, 384
+    x0 = torch.from_numpy(port.mixture(T * F, 4).reshape(T, F)).cuda().to(torch.bfloat16)
+    outs = {}
+    for transport in ("nccl", "peer"):
+        torch.manual_seed(0)
+        ctx = tp.TpContext(cfg=cfg, transport=transport)
+        row = tp.RowParallelLinear(F, H, ctx, device="cuda", dtype=torch.bfloat16)
+        col = tp.ColumnParallelLinear(H, F, ctx, device="cuda", dtype=torch.bfloat16)
+        x = x0.clone().requires_grad_(True)
+        y = col(row(x))
+        y.float().square().sum().backward()
+        rs = tp.reduce_scatter_to_sp(y.detach(), ctx)
+        ag = tp.gather_from_sp(rs, ctx)
+        outs[transport] = (y.detach(), x.grad, rs, ag)
+    for a, b in zip(outs["nccl"], outs["peer"]):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))

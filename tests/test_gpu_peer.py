@@ -54,6 +54,29 @@ def test_peer_schedule_sim_bit_identical(p, n, b, dtype):
         assert torch.equal(got[r].view(torch.int32), want.reshape(-1, n)[0].view(torch.int32)), f"rank {r}"
 
 
+@pytest.mark.parametrize("p,n,b,dtype", [(4, 8192 * 37 + 5, 256, torch.bfloat16), (3, 50_001, 64, torch.float32),
+                                          (8, 2560 * 64, 256, torch.bfloat16)])
+def test_peer_reduce_scatter_sim_bit_identical(p, n, b, dtype):
+    cfg = make_config(b)
+    ins = _inputs(p, n, dtype, 21 + p)
+    S = -(-n // p)
+    stage1 = torch.empty(p * S, dtype=torch.float32, device="cuda")
+    codec.allreduce_sim(ins, cfg, stage1=stage1)
+    got = peer.reduce_scatter_sim_peer(ins, cfg)
+    assert torch.equal(got.reshape(-1).view(torch.int32), stage1.view(torch.int32))
+
+
+@pytest.mark.parametrize("p,nl,b,dtype", [(4, 4096 * 9, 256, torch.bfloat16), (3, 10_007, 128, torch.float32),
+                                          (2, 65_536, 512, torch.bfloat16)])
+def test_peer_all_gather_sim_bit_identical(p, nl, b, dtype):
+    cfg = make_config(b)
+    ins = _inputs(p, nl, dtype, 31 + p)
+    want = torch.cat([codec.decompress(codec.compress(ins[r], cfg), nl, cfg) for r in range(p)])
+    got = peer.all_gather_sim_peer(ins, cfg)
+    for r in range(p):
+        assert torch.equal(got[r].view(torch.int32), want.view(torch.int32)), f"rank {r}"
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
