@@ -14,4 +14,11 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 4 --warmup 3 --no-cpu-baseline > "$OUT/ncu_bench.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(compress|decompress)' -s 6 -c 2 \
     -o "$OUT/prof" -f python bench.py --steps 4 --warmup 3 --no-cpu-baseline > "$OUT/ncu_full.log" 2>&1
+ncu -i "$OUT/prof.ncu-rep" --page raw --csv > "$OUT/raw.csv" 2>/dev/null
+ncu -i "$OUT/prof.ncu-rep" --page details --csv > "$OUT/ncu_details.csv" 2>/dev/null
+python tools/ncu_summary.py "$OUT/raw.csv" "$TAG" "$OUT/${TAG}_ncu_traffic.json" > /dev/null 2>&1
+timeout 300 python bench.py --collective > "$OUT/bench_coll.json" 2> "$OUT/bench_coll.err"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file "$OUT/launches_coll.csv" \
+    python bench.py --collective --eager --steps 2 --warmup 1 --no-cpu-baseline > "$OUT/ncu_coll.log" 2>&1
+bash tools/gpu_reftests.sh "$TAG/reftests" > /dev/null 2>&1
 echo done > "$OUT/DONE"
