@@ -40,6 +40,14 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+#ifndef TACO_TMA_ISSUE_FENCE
+#define TACO_TMA_ISSUE_FENCE 0  // proxy fence before every TMA refill: only needed after generic
+                                // writes to the slot (ragged tiles fence there); -3.5 % K2 fp32
+#endif
+#ifndef TACO_K2_MIN_CTAS
+#define TACO_K2_MIN_CTAS 5
+#endif
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -444,7 +452,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         const uint32_t p = tps.div(t);
         const uint64_t kk0 = (uint64_t)(t - p * tps.d) * kBlocks;
         if (tile_full<B, kBlocks>(a, p, kk0)) {
+#if TACO_TMA_ISSUE_FENCE
             fence_proxy_async();
+#endif
             mbar_arrive_tx(&bars[slot], Cf::STAGE);
             bulk_g2s(stage + slot * Cf::STAGE, x + (p * a.S + (a.blk0 + kk0) * B), Cf::STAGE, &bars[slot]);
         } else {
@@ -470,6 +480,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         if (!full) {
             fill_slow<NB, TIn>(st, x, a, p, kk0, lane);
             __syncwarp();
+            fence_proxy_async();  // these generic writes before any later TMA write of the slot
         }
         float2 w[Gm::E2];
         double ss;
@@ -583,7 +594,7 @@ __device__ __forceinline__ void stage_out(unsigned char* ob, const float2 (&w)[T
 }
 
 template <int NB, typename TOut>
-__global__ void __launch_bounds__(kTileWarps * 32, 5)
+__global__ void __launch_bounds__(kTileWarps * 32, TACO_K2_MIN_CTAS)
     k_decompress_tile(const uint8_t* __restrict__ msgs, TOut* __restrict__ out, ShardArgs a, CodecConsts c,
                       FastDiv tps) {
     using Gm = TG<NB>;
@@ -610,7 +621,9 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         const uint64_t kk0 = (uint64_t)(t - p * tps.d) * kBlocks;
         const uint8_t* m = msgs + p * a.msg_stride;
         if (kk0 + kBlocks <= a.nblk) {
+#if TACO_TMA_ISSUE_FENCE
             fence_proxy_async();
+#endif
             mbar_arrive_tx(&bars[slot], Cf::STAGE);
             unsigned char* st = stage + slot * Cf::STAGE;
             bulk_g2s(st, m + kk0 * B, Gm::TILE, &bars[slot]);
@@ -646,6 +659,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
                     kk0 + lane < a.nblk ? *reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + lane) * 8)
                                         : make_float2(1.0f, 1.0f);
             __syncwarp();
+            fence_proxy_async();  // these generic writes before any later TMA write of the slot
         }
         const float2 sc = reinterpret_cast<const float2*>(st + Gm::TILE)[g];
         float2 w[Gm::E2];
@@ -656,6 +670,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
         const bool full = tile_full<B, kBlocks>(a, p, kk0);
         TOut* dst = out + (p * a.S + (a.blk0 + kk0) * B);
         if (__all_sync(kFull, full)) {
+            // (direct 8-byte stores from the phase-2 registers measured 22.7 vs 18.5 us)
             __syncwarp();
             unsigned char* ob = reinterpret_cast<unsigned char*>(xb);
             stage_out<NB, TOut>(ob, w, g, q);
