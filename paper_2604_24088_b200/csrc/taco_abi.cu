@@ -676,9 +676,14 @@ int grow_host(void** bufs, size_t& cap, size_t need) {
     return TACO_OK;
 }
 
-// chunk = whole blocks, ~8 MiB of input per chunk
+// chunk = whole blocks, ~TACO_HOST_CHUNK_KB (default 8 MiB) of input per chunk
 uint64_t chunk_blocks(uint64_t b, size_t elt) {
-    const uint64_t target = (8ull << 20) / elt;
+    static const uint64_t bytes = [] {
+        const char* v = std::getenv("TACO_HOST_CHUNK_KB");
+        const long kb = v ? std::atol(v) : 0;
+        return kb > 0 ? (uint64_t)kb << 10 : (8ull << 20);
+    }();
+    const uint64_t target = bytes / elt;
     return std::max<uint64_t>(1, target / b);
 }
 

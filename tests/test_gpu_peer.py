@@ -32,16 +32,19 @@ def _inputs(p, n, dtype, seed):
     return x.to(dtype).cuda()
 
 
-@pytest.mark.parametrize("p,n,b,dtype", [
-    (2, 8192 * 40, 256, torch.bfloat16),        # tile K3, register K1
-    (4, 8192 * 37 + 5, 256, torch.float32),     # ragged last shard, tile K1
-    (8, 2560 * 64, 256, torch.bfloat16),        # the TP = 8 fan-out
-    (3, 100_003, 64, torch.bfloat16),           # register K3, odd P
-    (2, 65_536, 512, torch.float32),
-    (1, 4096 + 17, 256, torch.bfloat16),        # a group of one
+@pytest.mark.parametrize("p,n,b,dtype,fmt", [
+    (2, 8192 * 40, 256, torch.bfloat16, 0),        # tile K3, register K1
+    (4, 8192 * 37 + 5, 256, torch.float32, 0),     # ragged last shard, tile K1
+    (8, 2560 * 64, 256, torch.bfloat16, 0),        # the TP = 8 fan-out
+    (3, 100_003, 64, torch.bfloat16, 0),           # register K3, odd P
+    (2, 65_536, 512, torch.float32, 0),
+    (1, 4096 + 17, 256, torch.bfloat16, 0),        # a group of one
+    (4, 50_000, 256, torch.bfloat16, 1),           # E5M2 (fp64 rotation kernels)
+    (2, 30_000, 32, torch.float32, 0),             # small blocks
+    (3, 3 * 1024 * 9 + 1, 1024, torch.bfloat16, 0),  # the largest block the push path serves
 ])
-def test_peer_schedule_sim_bit_identical(p, n, b, dtype):
-    cfg = make_config(b)
+def test_peer_schedule_sim_bit_identical(p, n, b, dtype, fmt):
+    cfg = make_config(b, fmt)
     ins = _inputs(p, n, dtype, 11 + p)
     want = codec.allreduce_sim(ins, cfg) if p > 1 else None
     got = peer.allreduce_sim_peer(ins, cfg)
