@@ -94,10 +94,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
             const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
             auto* kern = &tile::k_compress_tile<NB, T>;
             const unsigned grid = persistent_grid(kern, tile::kTileWarps * 32, Cf::SMEM, tps * a.P, tile::kTileWarps);
-            kern<<<grid, tile::kTileWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in),
-                                                                      static_cast<uint8_t*>(l.out), a, c,
-                                                                      make_fastdiv((uint32_t)tps));
-            return cudaGetLastError();
+            return launch_k(kern, grid, tile::kTileWarps * 32, Cf::SMEM, l.stream, static_cast<const T*>(l.in),
+                            static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
         }
     }
     if constexpr (B <= 1024) {
@@ -106,7 +104,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = a.ndst ? &k_compress<B, T, FMT, EMAX, VMAX, true> : &k_compress<B, T, FMT, EMAX, VMAX, false>;
         const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
-        kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in), static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
+        return launch_k(kern, grid, kPipeWarps * 32, Cf::SMEM, l.stream, static_cast<const T*>(l.in),
+                        static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_compress_big<B, T, FMT>;

@@ -17,13 +17,11 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         if (kernel_family() != 2 && (tile || kernel_family() == 1)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K2T<NB, T>;
-            const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
+            const uint64_t tps = (a.nblk + Cf::KB - 1) / Cf::KB;
             auto* kern = &tile::k_decompress_tile<NB, T>;
             const unsigned grid = persistent_grid(kern, tile::kTileWarps * 32, Cf::SMEM, tps * a.P, tile::kTileWarps);
-            kern<<<grid, tile::kTileWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in),
-                                                                      static_cast<T*>(l.out), a, c,
-                                                                      make_fastdiv((uint32_t)tps));
-            return cudaGetLastError();
+            return launch_k(kern, grid, tile::kTileWarps * 32, Cf::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
+                            static_cast<T*>(l.out), a, c, make_fastdiv((uint32_t)tps));
         }
     }
     if constexpr (B <= 1024) {
@@ -32,7 +30,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = &k_decompress<B, T, FMT, EMAX, VMAX>;
         const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
-        kern<<<grid, kPipeWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in), static_cast<T*>(l.out), a, c, make_fastdiv((uint32_t)tps));
+        return launch_k(kern, grid, kPipeWarps * 32, Cf::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
+                        static_cast<T*>(l.out), a, c, make_fastdiv((uint32_t)tps));
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_decompress_big<B, T, FMT>;

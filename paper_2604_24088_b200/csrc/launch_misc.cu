@@ -244,6 +244,7 @@ __device__ __forceinline__ uint64_t globaltimer() {
 
 __global__ void k_peer_barrier(PeerSlots f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags) {
     __shared__ uint32_t e;
+    taco_dev::grid_dep_wait();  // the pushes of the kernel before this one have completed
     if (threadIdx.x == 0) {
         e = *f.epoch + 1;
         *f.epoch = e;
@@ -271,8 +272,7 @@ __global__ void k_peer_barrier(PeerSlots f, uint32_t rank, uint32_t P, uint64_t 
 
 cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags,
                                 cudaStream_t stream) {
-    k_peer_barrier<<<1, 32, 0, stream>>>(f, rank, P, timeout_ns, flags);
-    return cudaGetLastError();
+    return launch_k(&k_peer_barrier, dim3(1), dim3(32), 0, stream, f, rank, P, timeout_ns, flags);
 }
 
 }  // namespace taco_impl

@@ -22,10 +22,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
             }
             const uint64_t tiles = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
             const unsigned grid = (unsigned)((tiles + tile::kTileWarps - 1) / tile::kTileWarps);
-            kern<<<grid, tile::kTileWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const uint8_t*>(l.in),
-                                                                      static_cast<uint8_t*>(l.out),
-                                                                      static_cast<T*>(l.acc), a, c);
-            return cudaGetLastError();
+            return launch_k(kern, grid, tile::kTileWarps * 32, Cf::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
+                            static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
         }
     }
     if constexpr (B <= 1024) {
@@ -33,8 +31,9 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         // bits in the same order, so K3's per-rank decode is bit-identical to K2's
         constexpr int VMAX = 16, EMAX = FMT == 0 ? TACO_K2_EMAX : 32;
         using Gm = Geo<B, EMAX, VMAX>;
-        k_reduce_encode<B, T, FMT, EMAX, VMAX><<<warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads, 0, l.stream>>>(
-            static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
+        return launch_k(&k_reduce_encode<B, T, FMT, EMAX, VMAX>, warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads,
+                        0, l.stream, static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out),
+                        static_cast<T*>(l.acc), a, c);
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_reduce_encode_big<B, T, FMT>;

@@ -104,6 +104,16 @@ int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
 }  // namespace
 
 namespace taco_impl {
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("TACO_PDL");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+}  // namespace taco_impl
+
+namespace taco_impl {
 int kernel_family() {
     static const int fam = [] {
         const char* v = std::getenv("TACO_B200_KERNELS");

@@ -44,6 +44,14 @@ struct ShardArgs {
     uint32_t bcast = 0;  // K1 with ndst > 0: shard 0's message to every dst (all-gather)
 };
 
+// programmatic dependent launch (taco_launch.h launch_k): let the next kernel on the stream
+// be scheduled, then wait until the previous one has completed and its writes are visible.
+// Called before a kernel's first global memory access; a no-op without the launch attribute.
+__device__ __forceinline__ void grid_dep_wait() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 __device__ __forceinline__ uint8_t* shard_msg(uint8_t* msgs, const ShardArgs& a, uint64_t p) {
     return a.ndst ? a.dst[p] : msgs + p * a.msg_stride;
 }
@@ -198,6 +206,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
         cp_async_commit();  // possibly empty: keeps the group count uniform
     };
 
+    grid_dep_wait();
     if (t < ntiles) issue(t, 0);
     for (int it = 0; t < ntiles; t += stride, ++it) {
         if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
@@ -296,6 +305,7 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_decompress(co
         cp_async_commit();
     };
 
+    grid_dep_wait();
     if (t < ntiles) issue(t, 0);
     for (int it = 0; t < ntiles; t += stride, ++it) {
         const float2 sc = sc_next;
@@ -366,6 +376,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_reduce_encode(const uint8_t* _
     const bool live = kk < a.nblk;
     const uint64_t k = a.blk0 + kk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)B, B) : 0;
+    grid_dep_wait();
 
     RegsFor<FMT, E> acc;
     bool bad = false;

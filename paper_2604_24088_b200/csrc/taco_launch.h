@@ -74,6 +74,28 @@ struct PeerSlots {
 cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags,
                                 cudaStream_t stream);
 
+// Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous
+// kernel on the stream drains; it runs its prologue (shared-memory / mbarrier setup,
+// index math) and then blocks in griddepcontrol.wait until the previous grid has completed
+// and its memory is visible (taco_dev::grid_dep_wait, before ANY global access).  Hides
+// the launch gap and the ramp of back-to-back codec kernels.  TACO_PDL=0 disables it.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline taco_dev::FastDiv make_fastdiv(uint32_t d) {
     uint32_t s = 0;
     while ((1ull << s) < d) ++s;

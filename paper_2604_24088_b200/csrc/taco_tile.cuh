@@ -47,6 +47,9 @@ __device__ __forceinline__ void fence_mbar_init() {
 #ifndef TACO_K2_MIN_CTAS
 #define TACO_K2_MIN_CTAS 5
 #endif
+#ifndef TACO_K2_SUB
+#define TACO_K2_SUB 1  // 4-block sub-tiles per K2 TMA stage
+#endif
 
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kTileWarps * 32, 5)
             mbar_arrive(&bars[slot]);  // keeps the slot's phase sequence; filled by fill_slow
         }
     };
+    grid_dep_wait();
     if (lane == 0) {
 #pragma unroll
         for (int d = 0; d < D - 1; ++d)
@@ -516,7 +520,9 @@ template <int NB, typename TOut>
 struct K2T {
     using Gm = TG<NB>;
     static constexpr int D = 3;
-    static constexpr int STAGE = Gm::TILE + kBlocks * 8;  // codes + (alpha, s) of the tile
+    static constexpr int SUB = TACO_K2_SUB;                     // 4-block sub-tiles per TMA stage
+    static constexpr int KB = SUB * kBlocks;                    // blocks per stage
+    static constexpr int STAGE = SUB * (Gm::TILE + kBlocks * 8);  // [codes of KB blocks][their (alpha, s)]
     static constexpr int XB = Gm::TILE * 4;
     static constexpr int WARP_BYTES = D * STAGE + XB;
     static constexpr size_t SMEM = (size_t)kTileWarps * WARP_BYTES + (size_t)kTileWarps * D * 8;
@@ -616,22 +622,24 @@ __global__ void __launch_bounds__(kTileWarps * 32, TACO_K2_MIN_CTAS)
     const uint32_t stride = gridDim.x * kTileWarps;
     const uint32_t t0 = blockIdx.x * kTileWarps + warp;
 
+    constexpr int SUB = Cf::SUB, KB = Cf::KB, CODES = SUB * Gm::TILE;
     auto issue = [&](uint32_t t, int slot) {  // lane 0
         const uint32_t p = tps.div(t);
-        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * kBlocks;
+        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * KB;
         const uint8_t* m = msgs + p * a.msg_stride;
-        if (kk0 + kBlocks <= a.nblk) {
+        if (kk0 + KB <= a.nblk) {
 #if TACO_TMA_ISSUE_FENCE
             fence_proxy_async();
 #endif
             mbar_arrive_tx(&bars[slot], Cf::STAGE);
             unsigned char* st = stage + slot * Cf::STAGE;
-            bulk_g2s(st, m + kk0 * B, Gm::TILE, &bars[slot]);
-            bulk_g2s(st + Gm::TILE, m + a.scal_off + kk0 * 8, kBlocks * 8, &bars[slot]);
+            bulk_g2s(st, m + kk0 * B, CODES, &bars[slot]);
+            bulk_g2s(st + CODES, m + a.scal_off + kk0 * 8, KB * 8, &bars[slot]);
         } else {
             mbar_arrive(&bars[slot]);
         }
     };
+    grid_dep_wait();
     if (lane == 0) {
 #pragma unroll
         for (int d = 0; d < D - 1; ++d)
@@ -645,50 +653,55 @@ __global__ void __launch_bounds__(kTileWarps * 32, TACO_K2_MIN_CTAS)
         mbar_wait(&bars[slot], (par >> slot) & 1);
         par ^= 1u << slot;
         const uint32_t p = tps.div(t);
-        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * kBlocks;
+        const uint64_t kk0 = (uint64_t)(t - p * tps.d) * KB;
         unsigned char* st = stage + slot * Cf::STAGE;
         const uint8_t* m = msgs + p * a.msg_stride;
-        if (kk0 + kBlocks > a.nblk) {  // ragged tile: live blocks' codes, unit scalars elsewhere
-            for (int i = lane; i < Gm::TILE / 4; i += 32) {
+        if (kk0 + KB > a.nblk) {  // ragged stage: live blocks' codes, unit scalars elsewhere
+            for (int i = lane; i < CODES / 4; i += 32) {
                 const uint64_t kk = kk0 + (uint64_t)((4 * i) >> NB);
                 reinterpret_cast<uint32_t*>(st)[i] =
                     kk < a.nblk ? *reinterpret_cast<const uint32_t*>(m + kk0 * B + 4 * (uint64_t)i) : 0u;
             }
-            if (lane < kBlocks)
-                reinterpret_cast<float2*>(st + Gm::TILE)[lane] =
+            if (lane < KB)
+                reinterpret_cast<float2*>(st + CODES)[lane] =
                     kk0 + lane < a.nblk ? *reinterpret_cast<const float2*>(m + a.scal_off + (kk0 + lane) * 8)
                                         : make_float2(1.0f, 1.0f);
             __syncwarp();
             fence_proxy_async();  // these generic writes before any later TMA write of the slot
         }
-        const float2 sc = reinterpret_cast<const float2*>(st + Gm::TILE)[g];
-        float2 w[Gm::E2];
-        const bool ok = tile_decode<NB>(st, sc, xb, w, g, q, c);
-        const uint64_t kk = kk0 + g;
-        if (q == 0 && kk < a.nblk && !ok) raise_flag(a.flags, 2);
-        // whole tile valid and vector-aligned -> staged, coalesced 128-bit stores
-        const bool full = tile_full<B, kBlocks>(a, p, kk0);
-        TOut* dst = out + (p * a.S + (a.blk0 + kk0) * B);
-        if (__all_sync(kFull, full)) {
-            // (direct 8-byte stores from the phase-2 registers measured 22.7 vs 18.5 us)
-            __syncwarp();
-            unsigned char* ob = reinterpret_cast<unsigned char*>(xb);
-            stage_out<NB, TOut>(ob, w, g, q);
-            __syncwarp();
+#pragma unroll 1
+        for (int h = 0; h < SUB; ++h) {
+            const uint64_t kh = kk0 + (uint64_t)h * kBlocks;  // first block of the sub-tile
+            if (kh >= a.nblk) break;                          // warp-uniform
+            const float2 sc = reinterpret_cast<const float2*>(st + CODES)[h * kBlocks + g];
+            float2 w[Gm::E2];
+            const bool ok = tile_decode<NB>(st + h * Gm::TILE, sc, xb, w, g, q, c);
+            const uint64_t kk = kh + g;
+            if (q == 0 && kk < a.nblk && !ok) raise_flag(a.flags, 2);
+            // whole sub-tile valid and vector-aligned -> staged, coalesced 128-bit stores
+            const bool full = tile_full<B, kBlocks>(a, p, kh);
+            TOut* dst = out + (p * a.S + (a.blk0 + kh) * B);
+            if (__all_sync(kFull, full)) {
+                // (direct 8-byte stores from the phase-2 registers measured 22.7 vs 18.5 us)
+                __syncwarp();
+                unsigned char* ob = reinterpret_cast<unsigned char*>(xb);
+                stage_out<NB, TOut>(ob, w, g, q);
+                __syncwarp();
 #pragma unroll
-            for (int j = lane; j < Gm::TILE / EPC; j += 32) {
-                *reinterpret_cast<uint4*>(dst + (uint64_t)j * EPC) =
-                    *reinterpret_cast<const uint4*>(ob + 16 * swz((uint32_t)j));
-            }
-        } else if (kk < a.nblk) {
-            const uint64_t k = a.blk0 + kk;
-            const int valid =
-                clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
-            TOut* bd = out + (p * a.S + k * B);
+                for (int j = lane; j < Gm::TILE / EPC; j += 32) {
+                    *reinterpret_cast<uint4*>(dst + (uint64_t)j * EPC) =
+                        *reinterpret_cast<const uint4*>(ob + 16 * swz((uint32_t)j));
+                }
+            } else if (kk < a.nblk) {
+                const uint64_t k = a.blk0 + kk;
+                const int valid =
+                    clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
+                TOut* bd = out + (p * a.S + k * B);
 #pragma unroll
-            for (int r = 0; r < Gm::E; ++r) {
-                const int pos = Gm::pos2(r, q);
-                if (pos < valid) store_one(bd + pos, (r & 1) ? w[r / 2].y : w[r / 2].x);
+                for (int r = 0; r < Gm::E; ++r) {
+                    const int pos = Gm::pos2(r, q);
+                    if (pos < valid) store_one(bd + pos, (r & 1) ? w[r / 2].y : w[r / 2].x);
+                }
             }
         }
         slot = slot + 1 == D ? 0 : slot + 1;
@@ -764,6 +777,7 @@ __global__ void __launch_bounds__(kTileWarps * 32)
     float* xb = reinterpret_cast<float*>(slot + Cf::SLOT);
     const uint64_t tile = (uint64_t)blockIdx.x * kTileWarps + warp;
     const uint64_t kk0 = tile * kBlocks;
+    grid_dep_wait();
     if (kk0 >= a.nblk) return;  // warp-uniform
     const uint64_t kk = kk0 + g;
     const bool live = kk < a.nblk;
