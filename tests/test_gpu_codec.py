@@ -401,3 +401,35 @@ def test_allreduce_config_size_p2(port, big_input):
     ref = port.allreduce_twoshot(sub)["result"]
     got = np.concatenate([out[:k // 2], out[n // 2: n // 2 + k // 2]])
     assert rel_mse(got, ref) <= COLLECTIVE_RELMSE_MAX
+
+
+@pytest.mark.parametrize("dtype,b", [(torch.bfloat16, 256), (torch.float32, 256), (torch.bfloat16, 64)])
+def test_dependent_launch_chain_matches_synchronised_chain(port, dtype, b):
+    """K1/K2/K3 are launched with programmatic dependent launch (prologue overlaps the
+    previous kernel): a chain in which every launch reads the previous launch's output,
+    enqueued back to back, must equal the same chain with a host synchronise after every
+    launch (where no overlap is possible)."""
+    cfg = make_config(b)
+    n = 8192 * 96 + 77
+    x0 = torch.from_numpy(port.mixture(n, 17)).cuda().to(dtype)
+
+    def chain(sync):
+        y = x0
+        outs = []
+        for _ in range(6):
+            m = codec.compress(y, cfg, shards=2)
+            if sync:
+                torch.cuda.synchronize()
+            red = torch.empty_like(m[0])
+            codec.reduce_encode(m, 2, -(-n // 2), cfg, m.shape[1], red)
+            if sync:
+                torch.cuda.synchronize()
+            y = codec.decompress(m, n, cfg, shards=2, out_dtype=dtype)
+            if sync:
+                torch.cuda.synchronize()
+            outs += [m, red, y]
+        torch.cuda.synchronize()
+        return outs
+
+    for a, b_ in zip(chain(False), chain(True)):
+        assert torch.equal(a.view(torch.uint8), b_.view(torch.uint8))
