@@ -638,10 +638,13 @@ int taco_archive_parse_header(const uint8_t* bytes, uint64_t size, taco_config* 
 // with its neighbours' (two copy engines + SMs).  Pageable user memory is staged
 // through pinned slot buffers; pinned user memory is copied directly.
 
+// Host pipeline: three role streams (H2D, kernels, D2H) so the two copy engines stream
+// back to back; per-slot events order buffer reuse between them.
 struct taco_ctx {
     static constexpr int kSlots = 3;
     int device = 0;
-    cudaStream_t st[kSlots] = {};
+    cudaStream_t st[kSlots] = {};  // st[0] H2D, st[1] kernels, st[2] D2H
+    cudaEvent_t ev_in[kSlots] = {}, ev_k[kSlots] = {}, ev_out[kSlots] = {};
     void* d_in[kSlots] = {};
     void* d_msg[kSlots] = {};
     void* d_out[kSlots] = {};
@@ -712,8 +715,12 @@ int taco_ctx_create(int device, taco_ctx** out) {
     auto* c = new taco_ctx();
     c->device = device;
     cudaError_t e = cudaSetDevice(device);
-    for (int i = 0; i < taco_ctx::kSlots && e == cudaSuccess; ++i)
+    for (int i = 0; i < taco_ctx::kSlots && e == cudaSuccess; ++i) {
         e = cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_out[i], cudaEventDisableTiming);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&c->d_flags, sizeof(int));
     if (e != cudaSuccess) {
         delete c;
@@ -734,6 +741,9 @@ void taco_ctx_destroy(taco_ctx* c) {
         if (c->h_stage_in[i]) cudaFreeHost(c->h_stage_in[i]);
         if (c->h_stage_out[i]) cudaFreeHost(c->h_stage_out[i]);
         if (c->st[i]) cudaStreamDestroy(c->st[i]);
+        if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+        if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
+        if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
     }
     cudaFree(c->d_flags);
     delete c;
@@ -771,17 +781,37 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         if (int rc = grow_host(ctx->h_stage_in, ctx->cap_stage_in, in_bytes)) return rc;
     if (!pin_out)
         if (int rc = grow_host(ctx->h_stage_out, ctx->cap_stage_out, out_bytes)) return rc;
-    TACO_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), ctx->st[0]));
-    TACO_CUDA(cudaStreamSynchronize(ctx->st[0]));
+    cudaStream_t s_in = ctx->st[0], s_k = ctx->st[1], s_out = ctx->st[2];
+    TACO_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), s_k));
 
     const uint8_t* s8 = static_cast<const uint8_t*>(src);
     uint8_t* d8 = static_cast<uint8_t*>(dst);
-    const uint64_t nchunks = div_up(m, cb);
+    // chunk schedule: cb-block chunks, with the first and last ~1/8 of a chunk ramped
+    // (cb/8, cb/4, cb/2 ... cb/2, cb/4, cb/8) so the un-overlapped pipeline fill (first H2D)
+    // and drain (last kernels + D2H) are short; every chunk is whole blocks
+    std::vector<std::pair<uint64_t, uint64_t>> chunks;
+    {
+        std::vector<uint64_t> head, tail;
+        uint64_t left = m;
+        if (!whole && m >= 4 * cb)
+            for (uint64_t r = cb / 8; r >= 1 && r < cb; r *= 2) {
+                head.push_back(r);
+                tail.push_back(r);
+                left -= 2 * r;
+            }
+        uint64_t b0 = 0;
+        for (uint64_t r : head) chunks.push_back({b0, b0 + r}), b0 += r;
+        const uint64_t mid_end = b0 + left;
+        for (; b0 < mid_end; b0 += cb) chunks.push_back({b0, std::min(mid_end, b0 + cb)});
+        b0 = mid_end;
+        for (auto it = tail.rbegin(); it != tail.rend(); ++it) chunks.push_back({b0, b0 + *it}), b0 += *it;
+    }
+    const uint64_t nchunks = chunks.size();
     // staged output copies still in flight per slot: (host dst, bytes) pairs
     std::vector<std::pair<uint8_t*, size_t>> pending[taco_ctx::kSlots];
     auto drain = [&](int slot) -> int {
         if (pin_out || pending[slot].empty()) return TACO_OK;
-        TACO_CUDA(cudaStreamSynchronize(ctx->st[slot]));
+        TACO_CUDA(cudaEventSynchronize(ctx->ev_out[slot]));
         size_t off = 0;
         for (auto& pr : pending[slot]) {
             std::memcpy(pr.first, static_cast<uint8_t*>(ctx->h_stage_out[slot]) + off, pr.second);
@@ -792,20 +822,21 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
     };
     for (uint64_t ci = 0; ci < nchunks; ++ci) {
         const int slot = (int)(ci % taco_ctx::kSlots);
-        cudaStream_t st = ctx->st[slot];
-        const uint64_t b0 = ci * cb, b1 = std::min(m, b0 + cb), nb = b1 - b0;
+        const bool reuse = ci >= (uint64_t)taco_ctx::kSlots;
+        const uint64_t b0 = chunks[ci].first, b1 = chunks[ci].second, nb = b1 - b0;
         const uint64_t e0 = b0 * b, e1 = std::min<uint64_t>(n, b1 * b), ne = e1 - e0;
         const taco_layout lay = layout_of(pb, nb);
-        if (int rc = drain(slot)) return rc;  // slot buffers free again
-        if (!pin_in) TACO_CUDA(cudaStreamSynchronize(st));
-        // ---- H2D
+        if (int rc = drain(slot)) return rc;  // staged output of chunk ci - kSlots copied out
+        // ---- H2D (s_in): d_in[slot] is free once the kernels of chunk ci - kSlots ran
+        if (reuse) TACO_CUDA(cudaStreamWaitEvent(s_in, ctx->ev_k[slot], 0));
+        if (!pin_in && reuse) TACO_CUDA(cudaEventSynchronize(ctx->ev_in[slot]));  // staging slot free
         auto h2d = [&](void* d, const uint8_t* h, size_t bytes, size_t stage_off) -> int {
             if (pin_in) {
-                TACO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+                TACO_CUDA(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, s_in));
             } else {
                 uint8_t* stage = static_cast<uint8_t*>(ctx->h_stage_in[slot]) + stage_off;
                 std::memcpy(stage, h, bytes);
-                TACO_CUDA(cudaMemcpyAsync(d, stage, bytes, cudaMemcpyHostToDevice, st));
+                TACO_CUDA(cudaMemcpyAsync(d, stage, bytes, cudaMemcpyHostToDevice, s_in));
             }
             return TACO_OK;
         };
@@ -816,23 +847,29 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         } else {
             if (int rc = h2d(ctx->d_in[slot], s8 + e0 * ein, ne * ein, 0)) return rc;
         }
-        // ---- kernels (the chunk is a standalone tensor of ne elements: blocks never span chunks)
+        TACO_CUDA(cudaEventRecord(ctx->ev_in[slot], s_in));
+        // ---- kernels (s_k): the chunk is a standalone tensor of ne elements (blocks never
+        // span chunks); d_out[slot] is free once the D2H of chunk ci - kSlots finished
+        TACO_CUDA(cudaStreamWaitEvent(s_k, ctx->ev_in[slot], 0));
+        if (reuse) TACO_CUDA(cudaStreamWaitEvent(s_k, ctx->ev_out[slot], 0));
         void* msg = mode == 1 ? ctx->d_in[slot] : (mode == 0 ? ctx->d_out[slot] : ctx->d_msg[slot]);
         if (mode != 1)
             if (int rc = taco_compress_dev(cfg, ctx->d_in[slot], in_dtype, ne, 1, 0, nb, msg, lay.msg_stride,
-                                           ctx->d_flags, st))
+                                           ctx->d_flags, s_k))
                 return rc;
         if (mode != 0)
             if (int rc = taco_decompress_dev(cfg, msg, lay.msg_stride, 1, ne, 0, nb, ctx->d_out[slot], out_dtype,
-                                             ctx->d_flags, st))
+                                             ctx->d_flags, s_k))
                 return rc;
-        // ---- D2H
+        TACO_CUDA(cudaEventRecord(ctx->ev_k[slot], s_k));
+        // ---- D2H (s_out)
+        TACO_CUDA(cudaStreamWaitEvent(s_out, ctx->ev_k[slot], 0));
         auto d2h = [&](uint8_t* h, const void* d, size_t bytes, size_t stage_off) -> int {
             if (pin_out) {
-                TACO_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, st));
+                TACO_CUDA(cudaMemcpyAsync(h, d, bytes, cudaMemcpyDeviceToHost, s_out));
             } else {
                 uint8_t* stage = static_cast<uint8_t*>(ctx->h_stage_out[slot]) + stage_off;
-                TACO_CUDA(cudaMemcpyAsync(stage, d, bytes, cudaMemcpyDeviceToHost, st));
+                TACO_CUDA(cudaMemcpyAsync(stage, d, bytes, cudaMemcpyDeviceToHost, s_out));
                 pending[slot].push_back({h, bytes});
             }
             return TACO_OK;
@@ -844,6 +881,7 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
         } else {
             if (int rc = d2h(d8 + e0 * eout, ctx->d_out[slot], ne * eout, 0)) return rc;
         }
+        TACO_CUDA(cudaEventRecord(ctx->ev_out[slot], s_out));
     }
     for (int i = 0; i < taco_ctx::kSlots; ++i)
         if (int rc = drain(i)) return rc;

@@ -332,6 +332,30 @@ def test_host_api_matches_device_path(port):
     hc.close()
 
 
+def test_host_api_ramped_chunk_schedule(port):
+    """A tensor of > 4 pipeline chunks takes the ramped schedule (cb/8, cb/4, cb/2, cb ...,
+    cb/2, cb/4, cb/8 blocks): results identical to one device call, pinned or not."""
+    n = 9_000_000 + 123  # 36 MB of fp32: 4.3 chunks of 8 MiB
+    x = port.gaussian(n, 8)
+    cfg = make_config(256)
+    hc = codec.HostContext(0)
+    xd = torch.from_numpy(x).cuda()
+    msg_d = codec.compress(xd, cfg)
+    y_d = codec.decompress(msg_d, n, cfg).cpu().numpy()
+    lay = _abi.msg_layout(cfg, -(-n // 256))
+    msg_h = hc.compress(torch.from_numpy(x), cfg)
+    assert np.array_equal(msg_h.numpy(), msg_d[0, : lay.msg_bytes].cpu().numpy())
+    assert np.array_equal(hc.decompress(msg_h, n, cfg).numpy(), y_d)
+    for pin in (False, True):
+        xi = torch.from_numpy(x)
+        out = torch.empty(n, dtype=torch.float32)
+        if pin:
+            xi, out = xi.pin_memory(), out.pin_memory()
+        hc.roundtrip(xi, cfg, out)
+        assert np.array_equal(out.numpy(), y_d), f"pinned={pin}"
+    hc.close()
+
+
 # ------------------------------------------------------------------- allreduce (1 GPU) ---
 @pytest.mark.parametrize("name", golden_names("ar_"))
 def test_allreduce_sim_matches_reference_fixture(port, name):
