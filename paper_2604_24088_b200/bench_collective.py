@@ -41,6 +41,13 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
     except TacoError as e:
         return {"error": str(e)}
     pouts = [torch.empty_like(o) for o in outs]
+
+    def agree(ok: bool) -> bool:  # every rank takes the same branch (no mismatched collectives)
+        t = torch.tensor([1 if ok else 0], device=xs[0].device)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item() == 1)
+
+    err = ""
     try:
         graphs = [collective.Graphed(par, xs[i], pouts[i]) for i in range(R)] if not args.eager else None
 
@@ -54,24 +61,31 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
             pstep(i)
         torch.cuda.synchronize()
         par.check()
-        ms = _timed(pstep, args.steps, stream) / args.steps
-        par.check()
-        # bit-identical to the NCCL two-shot on the same input, on every rank
-        ar(xs[0], outs[0])
-        par(xs[0], pouts[0])
-        torch.cuda.synchronize()
-        par.check()
-        same = torch.tensor([1 if torch.equal(outs[0].view(torch.int16), pouts[0].view(torch.int16)) else 0],
-                            device=xs[0].device)
-        dist.all_reduce(same, op=dist.ReduceOp.MIN)
-        rep = {"ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
-               "speedup_vs_nccl_twoshot": round(step_ms / ms, 3),
-               "bit_identical_to_nccl_twoshot": bool(same.item() == 1),
-               "gpu_launches_per_step": 5, "barriers_per_step": 2}
     except TacoError as e:
-        rep = {"error": str(e)}
+        err = str(e)
+    if not agree(not err):
+        par.close()
+        return {"error": err or "failed on another rank"}
+    ms = _timed(pstep, args.steps, stream) / args.steps
+    # bit-identical to the NCCL two-shot on the same input, on every rank; errors are
+    # gathered, never raised between collectives
+    ar(xs[0], outs[0])
+    par(xs[0], pouts[0])
+    torch.cuda.synchronize()
+    try:
+        par.check()
+    except TacoError as e:
+        err = str(e)
+    same = torch.equal(outs[0].view(torch.int16), pouts[0].view(torch.int16))
+    t = torch.tensor([1 if same else 0, 0 if err else 1], device=xs[0].device)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
     par.close()
-    return rep
+    if int(t[1].item()) == 0:
+        return {"error": err or "failed on another rank"}
+    return {"ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
+            "speedup_vs_nccl_twoshot": round(step_ms / ms, 3),
+            "bit_identical_to_nccl_twoshot": bool(int(t[0].item()) == 1),
+            "gpu_launches_per_step": 5, "barriers_per_step": 2}
 
 
 def run_collective(args, rows, cols, clock_sampler, peaks):
