@@ -41,8 +41,16 @@ def main():
                                            m, C.c_void_p(ys[i].data_ptr()), dcode, None, sp))
 
     c = 1 + 8 / b
+
+    def rt(i):
+        k1(i)
+        k2(i)
+
+    kernels = [("k1_compress", k1, esz + c), ("k2_decompress", k2, c + esz)]
+    if os.environ.get("RT"):
+        kernels.append(("roundtrip", rt, 2 * (esz + c)))
     with torch.cuda.stream(st):
-        for name, fn, bpe in (("k1_compress", k1, esz + c), ("k2_decompress", k2, c + esz)):
+        for name, fn, bpe in kernels:
             for i in range(8):
                 k1(i % R)
                 fn(i % R)
