@@ -104,8 +104,13 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = a.ndst ? &k_compress<B, T, FMT, EMAX, VMAX, true> : &k_compress<B, T, FMT, EMAX, VMAX, false>;
         const unsigned grid = persistent_grid(kern, kPipeWarps * 32, Cf::SMEM, tps * a.P, kPipeWarps);
+        uint32_t* ctr = nullptr;
+        if (k1_dynamic()) {
+            ctr = claim_counter();
+            if (!ctr) return cudaErrorMemoryAllocation;
+        }
         return launch_k(kern, grid, kPipeWarps * 32, Cf::SMEM, l.stream, static_cast<const T*>(l.in),
-                        static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
+                        static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps), ctr);
     } else {
         const size_t smem = (size_t)B * sizeof(BigW<FMT, B>);
         auto* kern = &k_compress_big<B, T, FMT>;

@@ -104,6 +104,13 @@ int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
 }  // namespace
 
 namespace taco_impl {
+bool k1_dynamic() {
+    static const bool on = [] {
+        const char* v = std::getenv("TACO_K1_DYNAMIC");
+        return v && std::strcmp(v, "1") == 0;
+    }();
+    return on;
+}
 bool pdl_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("TACO_PDL");

@@ -12,6 +12,9 @@
 
 #include "taco_device.cuh"
 
+#ifndef TACO_K1_WARP_MAJOR
+#define TACO_K1_WARP_MAJOR 0
+#endif
 #ifndef TACO_FAST_SCALARS_REG
 #define TACO_FAST_SCALARS_REG 1  // branch-free scalar chain (+2.5 % K1, profiles/README.md)
 #endif
@@ -175,9 +178,15 @@ struct K1Cfg {
 // --------------------------------------------------------------------------- K1 ---
 // PUSH: peer-memory mode (ShardArgs::dst), a separate instantiation so the default
 // kernel keeps its register allocation
+// ctr (optional): dynamic schedule -- each warp's first tile is static (t < nwarps), later
+// tiles are claimed from a per-launch counter one tile ahead of the prefetch, so warps
+// that finish early take more work instead of idling through the static 4-vs-5-tile tail.
+// Every warp makes exactly two failed claims; the claim that returns the last raw value
+// resets the counter for the next launch that draws the same ring slot.
 template <int B, typename TIn, int FMT, int EMAX, int VMAX, bool PUSH = false>
 __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(const TIn* __restrict__ x, uint8_t* __restrict__ msgs,
-                                                              ShardArgs a, CodecConsts c, FastDiv tps) {
+                                                              ShardArgs a, CodecConsts c, FastDiv tps,
+                                                              uint32_t* __restrict__ ctr) {
     using Cf = K1Cfg<B, TIn, FMT, EMAX, VMAX>;
     using Gm = typename Cf::Gm;
     constexpr int E = Gm::E, V = Gm::V, L = Gm::L, G = Gm::G, NV = Gm::NV, CPV = Cf::CPV;
@@ -187,7 +196,13 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
     uint4* stage_base = smem_dyn + (size_t)warp * 2 * Cf::STAGE_U4;
     const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kPipeWarps;
+#if TACO_K1_WARP_MAJOR
+    // warp-major numbering: the warps that get one tile more than the others (tiles do not
+    // divide evenly) are spread over all SMs instead of piling onto the first CTAs' SMs
+    uint32_t t = warp * gridDim.x + blockIdx.x;
+#else
     uint32_t t = blockIdx.x * kPipeWarps + warp;
+#endif
 
     auto issue = [&](uint32_t tt, int stage) {
         if constexpr (Cf::PIPE) {
@@ -207,9 +222,21 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
     };
 
     grid_dep_wait();
+    const uint32_t last_raw = (ntiles > stride ? ntiles - stride : 0u) + 2u * stride - 1u;
+    auto claim = [&]() -> uint32_t {  // lane 0's raw claim (other lanes: 0)
+        uint32_t r = 0;
+        if (lane == 0) {
+            r = atomicAdd(ctr, 1u);
+            if (r == last_raw) atomicExch(ctr, 0u);
+        }
+        return r;
+    };
+    uint32_t tn = ctr ? stride + __shfl_sync(kFull, claim(), 0) : t + stride;  // the tile after t
     if (t < ntiles) issue(t, 0);
-    for (int it = 0; t < ntiles; t += stride, ++it) {
-        if (t + stride < ntiles) issue(t + stride, (it + 1) & 1);
+    else if (ctr) claim();  // an idle warp still makes its two failed claims
+    for (int it = 0; t < ntiles; ++it) {
+        const uint32_t pend = ctr ? claim() : 0u;  // the tile after tn (used next iteration)
+        if (tn < ntiles) issue(tn, (it + 1) & 1);
         else cp_async_commit();
         const uint32_t p = tps.div(t);
         const uint64_t kk0 = (uint64_t)(t - p * tps.d) * G;
@@ -258,6 +285,8 @@ __global__ void __launch_bounds__(kPipeWarps * 32, kPipeMinCtas) k_compress(cons
             }
             if (q == 0 && !isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
         }
+        t = tn;
+        tn = ctr ? stride + __shfl_sync(kFull, pend, 0) : tn + stride;
     }
 }
 

@@ -80,6 +80,8 @@ cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, u
 // and its memory is visible (taco_dev::grid_dep_wait, before ANY global access).  Hides
 // the launch gap and the ramp of back-to-back codec kernels.  TACO_PDL=0 disables it.
 bool pdl_enabled();
+// register K1 tile schedule: dynamic claims (TACO_K1_DYNAMIC=1) or static round robin
+bool k1_dynamic();
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
