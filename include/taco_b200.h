@@ -150,6 +150,25 @@ int taco_allreduce_sim_dev(const taco_config* cfg, const void* inputs, int dtype
 int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
                              float* out, int* d_flags, void* stream);
 
+/* --------------------------------------------- collectives over a caller's NCCL communicator ---
+ * The two-shot across real ranks (collective.cpp:75-111; SURVEY §8b taco_allreduce_twoshot),
+ * one rank per GPU: K1 -> grouped ncclSend/ncclRecv (all-to-all of the FP8 messages) -> K3
+ * -> ncclAllGather -> K2, all on `stream`.  `comm` is an ncclComm_t of P ranks (P = the shard
+ * count); NCCL is resolved at run time from the process (the library does not link it).
+ * work: taco_collective_nccl_workspace(cfg, P, n_total) bytes of device memory, n_total =
+ * the full tensor (all-gather: P * n_local). */
+uint64_t taco_collective_nccl_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n_total);
+/* all-reduce: x[n] (dtype) -> out[n] (out_dtype), identical on every rank */
+int taco_allreduce_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out, int out_dtype,
+                        void* work, void* comm, int* d_flags, void* stream);
+/* sequence-parallel reduce-scatter: x[n] -> this rank's shard out[ceil(n/P)], the ascending-
+ * rank fp32 sum of the decoded shard copies (collective.cpp:95-100), in out_dtype */
+int taco_reduce_scatter_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
+                             int out_dtype, void* work, void* comm, int* d_flags, void* stream);
+/* sequence-parallel all-gather: x[n_local] -> out[P * n_local] (every rank's slice decoded) */
+int taco_all_gather_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n_local, void* out,
+                         int out_dtype, void* work, void* comm, int* d_flags, void* stream);
+
 /* ------------------------------------ peer-memory two-shot (SURVEY §8e, B200 extras) -----
  * The two-shot of collective.cpp:75-111 with the exchange folded into the kernels, no
  * NCCL call on the data path: K1 stores shard p's message straight into rank p's

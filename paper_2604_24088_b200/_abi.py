@@ -112,6 +112,10 @@ _SIGNATURES = {
     "taco_archive_import_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P, _P]),
     "taco_scaled_spectrum_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P]),
     "taco_error_report_dev": (C.c_int, [_P, _I, _P, _I, _U64, _U32, C.POINTER(ErrorReportC), _P, _P]),
+    "taco_collective_nccl_workspace": (_U64, [C.POINTER(Config), _U32, _U64]),
+    "taco_allreduce_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
+    "taco_reduce_scatter_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
+    "taco_all_gather_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_peer_alloc": (C.c_int, [_I, _U64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
     "taco_peer_open": (C.c_int, [_I, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),
     "taco_peer_close": (C.c_int, [_P]),

@@ -104,6 +104,10 @@ int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
 }  // namespace
 
 namespace taco_impl {
+int set_error(int code, const char* msg) { return fail(code, msg); }
+}  // namespace taco_impl
+
+namespace taco_impl {
 bool k1_dynamic() {
     static const bool on = [] {
         const char* v = std::getenv("TACO_K1_DYNAMIC");
