@@ -135,6 +135,15 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
                            uint64_t blk_end, void* out_msg, void* acc_out, int acc_dtype,
                            int* d_flags, void* stream);
 
+/* K3 with the P rank messages at arbitrary device addresses (SURVEY §8b
+ * taco_decode_reduce_encode(const uint8_t* const* in, int P, ...)): msgs is a HOST array of
+ * nranks (<= TACO_MAX_PEERS) device pointers, each a message of blk_end - blk_begin blocks
+ * (e.g. the peers' send buffers mapped over NVLink: a pull-style owner reduction).  Same
+ * results as taco_reduce_encode_dev on the same bytes.  B <= 1024. */
+int taco_reduce_encode_ptrs_dev(const taco_config* cfg, const void* const* msgs, uint32_t nranks,
+                                uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end, void* out_msg,
+                                void* acc_out, int acc_dtype, int* d_flags, void* stream);
+
 /* In-process P-rank two-shot all-reduce on ONE device: the reference's RankSet
  * simulation (taco::allreduce, collective.hpp:28, Algorithm::TwoShot,
  * collective.cpp:75-111) with every "rank" a slice of `inputs` ([P][n], dtype).

@@ -97,6 +97,8 @@ _SIGNATURES = {
     "taco_decompress_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _U32, _U64, _U64, _U64, _P, _I, _P, _P]),
     "taco_reduce_encode_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _U32, _U64, _U64, _U64, _P, _P, _I,
                                          _P, _P]),
+    "taco_reduce_encode_ptrs_dev": (C.c_int, [C.POINTER(Config), C.POINTER(C.c_void_p), _U32, _U64, _U64, _U64, _P,
+                                              _P, _I, _P, _P]),
     "taco_allreduce_sim_workspace": (_U64, [C.POINTER(Config), _U32, _U64]),
     "taco_allreduce_sim_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U32, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_ctx_create": (C.c_int, [C.c_int, C.POINTER(C.c_void_p)]),

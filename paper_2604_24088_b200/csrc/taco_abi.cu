@@ -463,6 +463,36 @@ int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64
     return TACO_OK;
 }
 
+int taco_reduce_encode_ptrs_dev(const taco_config* cfg, const void* const* msgs, uint32_t nranks,
+                                uint64_t shard_len, uint64_t blk_begin, uint64_t blk_end, void* out_msg, void* acc_out,
+                                int acc_dtype, int* d_flags, void* stream) {
+    if (!msgs) return fail(TACO_ERR_USAGE, "null message pointer array");
+    if (nranks == 0 || nranks > TACO_MAX_PEERS) return fail(TACO_ERR_USAGE, "pointer-array reduction takes 1 to 8 ranks");
+    for (uint32_t r = 0; r < nranks; ++r)
+        if (!msgs[r]) return fail(TACO_ERR_USAGE, "null message pointer");
+    if (int rc = check_config(cfg)) return rc;
+    if (acc_out)
+        if (int rc = check_dtype(acc_dtype)) return rc;
+    if (!out_msg && !acc_out) return fail(TACO_ERR_USAGE, "reduce-encode needs out_msg or acc_out");
+    if (shard_len == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (cfg->kind != 0)
+        return fail(TACO_ERR_USAGE, "the fused reduce-encode serves CodecKind::Taco (use decompress + compress)");
+    const uint64_t b = cfg->block_size, m = div_up(shard_len, b);
+    if (int rc = check_range(m, blk_begin, blk_end)) return rc;
+    if (b > 1024) return fail(TACO_ERR_USAGE, "pointer-array reduction supports block sizes up to 1024");
+    const taco_layout lay = layout_of(b, blk_end - blk_begin);
+    ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset,
+                acc_out ? aligned16(acc_out) : 0, d_flags};
+    taco_dev::with_full_blocks(a, b);
+    a.full_last = a.full_mid;
+    for (uint32_t r = 0; r < nranks; ++r) a.src[r] = static_cast<const uint8_t*>(msgs[r]);
+    a.nsrc = nranks;
+    Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs[0], out_msg, acc_out, (cudaStream_t)stream};
+    if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
+        return cuda_fail(e, "K3 reduce-encode launch");
+    return TACO_OK;
+}
+
 uint64_t taco_allreduce_sim_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n) {
     if (!cfg || nranks == 0 || n == 0) return 0;
     const uint64_t S = div_up(n, nranks);

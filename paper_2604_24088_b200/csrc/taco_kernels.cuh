@@ -45,6 +45,10 @@ struct ShardArgs {
     uint8_t* dst[kMaxPeers] = {};
     uint32_t ndst = 0;
     uint32_t bcast = 0;  // K1 with ndst > 0: shard 0's message to every dst (all-gather)
+    // K3 with nsrc > 0: rank r's message is read from src[r] (any address, e.g. a peer's
+    // buffer over NVLink) instead of msgs + r * msg_stride
+    const uint8_t* src[kMaxPeers] = {};
+    uint32_t nsrc = 0;
 };
 
 // programmatic dependent launch (taco_launch.h launch_k): let the next kernel on the stream
@@ -410,7 +414,7 @@ __global__ void __launch_bounds__(kWarpThreads) k_reduce_encode(const uint8_t* _
     RegsFor<FMT, E> acc;
     bool bad = false;
     for (uint32_t r = 0; r < a.P; ++r) {
-        const uint8_t* m = msgs + r * a.msg_stride;
+        const uint8_t* m = a.nsrc ? a.src[r] : msgs + r * a.msg_stride;
         RegsFor<FMT, E> d;
         float2 sc = make_float2(1.0f, 1.0f);
         if (live) {

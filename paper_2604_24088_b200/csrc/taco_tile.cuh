@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(kTileWarps * 32)
     uint4 pre[Cf::PER_LANE];
     float2 pre_sc = make_float2(1.0f, 1.0f);
     auto fetch = [&](uint32_t r) {
-        const uint8_t* m = msgs + r * a.msg_stride;
+        const uint8_t* m = a.nsrc ? a.src[r] : msgs + r * a.msg_stride;
 #pragma unroll
         for (int h = 0; h < Cf::PER_LANE; ++h) {
             const int i = lane + 32 * h;

@@ -169,3 +169,30 @@ def test_tp_peer_transport_matches_nccl(port, nccl_world1):
         outs[transport] = (y.detach(), x.grad, rs, ag)
     for a, b in zip(outs["nccl"], outs["peer"]):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+@pytest.mark.parametrize("b,P", [(256, 2), (256, 8), (64, 3), (512, 5), (128, 1)])
+def test_reduce_encode_pointer_array_matches_strided(port, b, P):
+    """taco_reduce_encode_ptrs_dev (rank messages at arbitrary addresses) gives the
+    same bytes and stage-1 sums as the strided K3 on the same messages."""
+    import ctypes as C
+    cfg = make_config(b)
+    n = P * 40_000 + 7
+    x = torch.from_numpy(port.mixture(n, 3 + P)).cuda().to(torch.bfloat16)
+    msgs = codec.compress(x, cfg, shards=P)  # P messages of one shard geometry
+    S = -(-n // P)
+    m = -(-S // b)
+    lay = _abi.msg_layout(cfg, m)
+    copies = [msgs[r].clone() for r in range(P)]  # separate allocations
+    want = torch.zeros(lay.msg_stride, dtype=torch.uint8, device="cuda")
+    acc_w = torch.empty(S, dtype=torch.float32, device="cuda")
+    codec.reduce_encode(msgs, P, S, cfg, lay.msg_stride, want, acc_out=acc_w)
+    got = torch.zeros_like(want)
+    acc_g = torch.empty_like(acc_w)
+    ptrs = (C.c_void_p * P)(*[c.data_ptr() for c in copies])
+    _abi.check(_abi.lib().taco_reduce_encode_ptrs_dev(C.byref(cfg), ptrs, P, S, 0, m, C.c_void_p(got.data_ptr()),
+                                                      C.c_void_p(acc_g.data_ptr()), _abi.DT_F32, None,
+                                                      C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    torch.cuda.synchronize()
+    assert torch.equal(got[: lay.msg_bytes], want[: lay.msg_bytes])
+    assert torch.equal(acc_g.view(torch.int32), acc_w.view(torch.int32))
