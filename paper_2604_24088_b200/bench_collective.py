@@ -117,7 +117,22 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(R)]
     ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=dev)
     stream = torch.cuda.current_stream()
-    graphs = [collective.Graphed(ar, xs[i], outs[i]) for i in range(R)] if not args.eager else None
+    graphs, launch_note = None, "eager"
+    if not args.eager:
+        # CUDA-graph capture of the step (kernels + NCCL); every rank takes the same path
+        try:
+            graphs = [collective.Graphed(ar, xs[i], outs[i]) for i in range(R)]
+            ok = 1
+        except Exception as e:  # noqa: BLE001 -- reported in the JSON line, eager instead
+            graphs, ok, launch_note = None, 0, f"eager (graph capture failed: {type(e).__name__})"
+        t = torch.tensor([ok], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        if int(t.item()) == 1:
+            launch_note = "cuda_graph"
+        else:
+            graphs = None
+            if launch_note == "eager":
+                launch_note = "eager (graph capture failed on another rank)"
 
     def step(i):
         if graphs is not None:
@@ -159,7 +174,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     yh = torch.empty(n, dtype=torch.bfloat16).pin_memory()
     xd = torch.empty_like(xs[0])
 
-    g_e2e = collective.Graphed(ar, xd, outs[0]) if not args.eager else None
+    g_e2e = collective.Graphed(ar, xd, outs[0]) if graphs is not None else None
 
     def e2e_step(i):
         xd.copy_(xh, non_blocking=True)
@@ -199,7 +214,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
             "config": {"workload": f"configs[1] tensor per rank, TP={world} FP8 two-shot all-reduce",
                        "shape": [rows, cols], "elements_per_rank": n, "block_size": args.block_size,
                        "format": "E4M3", "chunks": args.chunks, "parallelism": f"tp{world}",
-                       "launch": "eager" if args.eager else "cuda_graph",
+                       "launch": launch_note,
                        "l2": f"{R} rotating input/output buffers of {2 * n / 1e6:.0f} MB"},
             "nccl_bf16_allreduce": {"ms_per_step": round(nccl_ms, 5),
                                     "algbw_GBps": round(world * 2 * n / (nccl_ms * 1e-3) / 1e9, 1),
