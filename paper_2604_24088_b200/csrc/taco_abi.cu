@@ -38,6 +38,20 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call);    \
     } while (0)
 
+// Switches the calling thread to `device` for the scope and restores the caller's device
+// on exit: host entry points must not leave the caller's current device changed.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != device) err = cudaSetDevice(device);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 bool pow2(uint64_t b) { return b != 0 && (b & (b - 1)) == 0; }
 
 uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
@@ -316,7 +330,8 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
 int taco_peer_alloc(int device, uint64_t bytes, void** ptr, taco_ipc_handle* handle) {
     static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(taco_ipc_handle), "IPC handle size");
     if (!ptr || !handle || bytes == 0) return fail(TACO_ERR_USAGE, "peer allocation needs a size and outputs");
-    TACO_CUDA(cudaSetDevice(device));
+    DeviceGuard dg(device);
+    TACO_CUDA(dg.err);
     void* p = nullptr;
     TACO_CUDA(cudaMalloc(&p, bytes));
     cudaIpcMemHandle_t h;
@@ -334,7 +349,8 @@ int taco_peer_alloc(int device, uint64_t bytes, void** ptr, taco_ipc_handle* han
 
 int taco_peer_open(int device, const taco_ipc_handle* handle, void** ptr) {
     if (!ptr || !handle) return fail(TACO_ERR_USAGE, "peer open needs a handle");
-    TACO_CUDA(cudaSetDevice(device));
+    DeviceGuard dg(device);
+    TACO_CUDA(dg.err);
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle->bytes, sizeof(h));
     TACO_CUDA(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
@@ -755,7 +771,8 @@ extern "C" {
 int taco_ctx_create(int device, taco_ctx** out) {
     auto* c = new taco_ctx();
     c->device = device;
-    cudaError_t e = cudaSetDevice(device);
+    DeviceGuard dg(device);
+    cudaError_t e = dg.err;
     for (int i = 0; i < taco_ctx::kSlots && e == cudaSuccess; ++i) {
         e = cudaStreamCreateWithFlags(&c->st[i], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming);
@@ -773,7 +790,7 @@ int taco_ctx_create(int device, taco_ctx** out) {
 
 void taco_ctx_destroy(taco_ctx* c) {
     if (!c) return;
-    cudaSetDevice(c->device);
+    DeviceGuard dg(c->device);
     for (int i = 0; i < taco_ctx::kSlots; ++i) {
         if (c->st[i]) cudaStreamSynchronize(c->st[i]);
         cudaFree(c->d_in[i]);
@@ -802,7 +819,8 @@ static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const 
     if (n == 0) return mode == 1 ? fail(TACO_ERR_CORRUPT, "compressed tensor declares zero elements")
                                  : fail(TACO_ERR_INPUT, "input tensor is empty");
     std::lock_guard<std::mutex> lock(ctx->mu);
-    TACO_CUDA(cudaSetDevice(ctx->device));
+    DeviceGuard dg(ctx->device);
+    TACO_CUDA(dg.err);
     const uint64_t b = cfg->block_size, m = div_up(n, b), pb = payload_of(cfg);
     const size_t ein = mode == 1 ? 1 : dtype_size(in_dtype);
     const size_t eout = mode == 0 ? 1 : dtype_size(out_dtype);
@@ -950,7 +968,8 @@ int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float
     if (int rc = check_config(cfg)) return rc;
     if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
     std::lock_guard<std::mutex> lock(ctx->mu);
-    TACO_CUDA(cudaSetDevice(ctx->device));
+    DeviceGuard dg(ctx->device);
+    TACO_CUDA(dg.err);
     const uint64_t out_n = div_up(n, cfg->block_size) * cfg->block_size;
     void *d_in = nullptr, *d_out = nullptr;
     cudaStream_t st = ctx->st[0];
@@ -983,7 +1002,8 @@ int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* 
     if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
     if (int rc = check_config(cfg)) return rc;
     std::lock_guard<std::mutex> lock(ctx->mu);
-    TACO_CUDA(cudaSetDevice(ctx->device));
+    DeviceGuard dg(ctx->device);
+    TACO_CUDA(dg.err);
     const uint64_t S = div_up(n, nranks);
     const size_t in_bytes = (size_t)nranks * n * 4, st_bytes = stage1_host ? (size_t)nranks * S * 4 : 0;
     const size_t ws = taco_allreduce_sim_workspace(cfg, nranks, n);
