@@ -98,7 +98,9 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
                             static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
         }
     }
-    if constexpr (B <= 1024) {
+    // E4M3 B = 2048: one warp per block (32 lanes x 64 values, 5 shuffle stages) instead of
+    // the CTA-per-block shared-memory kernel
+    if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {
         constexpr int VMAX = 8, EMAX = FMT == 0 ? TACO_K1_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
         using Cf = K1Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;

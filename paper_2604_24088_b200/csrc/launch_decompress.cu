@@ -24,8 +24,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
                             static_cast<T*>(l.out), a, c, make_fastdiv((uint32_t)tps));
         }
     }
-    if constexpr (B <= 1024) {
-        constexpr int VMAX = 16, EMAX = FMT == 0 ? TACO_K2_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
+    if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {  // B = 2048: one warp per block
+        constexpr int VMAX = 16, EMAX = FMT == 0 ? (B == 2048 ? 64 : TACO_K2_EMAX) : 32;
         using Cf = K2Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = &k_decompress<B, T, FMT, EMAX, VMAX>;
