@@ -9,6 +9,29 @@
 
 #include <mutex>
 
+// values per lane of the register K1 (E4M3), per block size -- measured, bf16 [8192x2560]:
+// B = 64: 32 -> 19.6 us (64 -> 29.4); B = 128: 32 -> 19.2 us (64 -> 22.2)
+#ifndef TACO_K1_EMAX_B64
+#define TACO_K1_EMAX_B64 32
+#endif
+#ifndef TACO_K1_EMAX_B128
+#define TACO_K1_EMAX_B128 32
+#endif
+#ifndef TACO_K1_EMAX_B256
+#define TACO_K1_EMAX_B256 TACO_K1_EMAX
+#endif
+#ifndef TACO_K1_EMAX_B512
+#define TACO_K1_EMAX_B512 TACO_K1_EMAX
+#endif
+#ifndef TACO_K1_EMAX_B1024
+#define TACO_K1_EMAX_B1024 TACO_K1_EMAX
+#endif
+template <int B>
+constexpr int k1_emax() {
+    return B == 64 ? TACO_K1_EMAX_B64 : B == 128 ? TACO_K1_EMAX_B128 : B == 256 ? TACO_K1_EMAX_B256
+         : B == 512 ? TACO_K1_EMAX_B512 : B == 1024 ? TACO_K1_EMAX_B1024 : TACO_K1_EMAX;
+}
+
 namespace taco_impl {
 using namespace taco_dev;
 
@@ -88,7 +111,9 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
         const int fam = kernel_family();
-        if (fam == 1 || (fam == 0 && std::is_same<T, float>::value)) {
+        // fp32 input: the tile kernel for 128 <= B <= 512; at B = 64 the register kernel
+        // (31.8 vs 41.3 us, profiles/README.md)
+        if (fam == 1 || (fam == 0 && std::is_same<T, float>::value && B >= 128)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K1T<NB, T>;
             const uint64_t tps = (a.nblk + tile::kBlocks - 1) / tile::kBlocks;
@@ -101,7 +126,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     // E4M3 B = 2048: one warp per block (32 lanes x 64 values, 5 shuffle stages) instead of
     // the CTA-per-block shared-memory kernel
     if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {
-        constexpr int VMAX = 8, EMAX = FMT == 0 ? TACO_K1_EMAX : 32;  // fp32 pairs: 64/lane; fp64: 32/lane
+        constexpr int VMAX = 8, EMAX = FMT == 0 ? k1_emax<B>() : 32;
         using Cf = K1Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = a.ndst ? &k_compress<B, T, FMT, EMAX, VMAX, true> : &k_compress<B, T, FMT, EMAX, VMAX, false>;
