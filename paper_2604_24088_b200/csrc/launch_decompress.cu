@@ -25,7 +25,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         }
     }
     if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {  // B = 2048: one warp per block
-        constexpr int VMAX = 16, EMAX = FMT == 0 ? (B == 2048 ? 64 : TACO_K2_EMAX) : 32;
+        constexpr int VMAX = 16, EMAX = FMT == 0 ? k2_emax<B>() : 32;
         using Cf = K2Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = &k_decompress<B, T, FMT, EMAX, VMAX>;

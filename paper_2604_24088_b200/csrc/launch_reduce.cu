@@ -29,7 +29,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {
         // the decode geometry of K2 (launch_decompress.cu): fp32 butterflies over the same
         // bits in the same order, so K3's per-rank decode is bit-identical to K2's
-        constexpr int VMAX = 16, EMAX = FMT == 0 ? (B == 2048 ? 64 : TACO_K2_EMAX) : 32;
+        constexpr int VMAX = 16, EMAX = FMT == 0 ? k2_emax<B>() : 32;
         using Gm = Geo<B, EMAX, VMAX>;
         return launch_k(&k_reduce_encode<B, T, FMT, EMAX, VMAX>, warp_grid(a.nblk, Gm::G, kWarpThreads), kWarpThreads,
                         0, l.stream, static_cast<const uint8_t*>(l.in), static_cast<uint8_t*>(l.out),

@@ -74,6 +74,19 @@ struct PeerSlots {
 cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, uint64_t timeout_ns, int* flags,
                                 cudaStream_t stream);
 
+// values per lane of the register K2 / K3 decode (E4M3), per block size: K3 decodes with
+// exactly K2's geometry so its stage-1 sums are bit-identical to K2 decodes
+#ifndef TACO_K2_EMAX_B64
+#define TACO_K2_EMAX_B64 TACO_K2_EMAX
+#endif
+#ifndef TACO_K2_EMAX_B1024
+#define TACO_K2_EMAX_B1024 TACO_K2_EMAX
+#endif
+template <int B>
+constexpr int k2_emax() {
+    return B == 2048 ? 64 : B == 64 ? TACO_K2_EMAX_B64 : B == 1024 ? TACO_K2_EMAX_B1024 : TACO_K2_EMAX;
+}
+
 // Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous
 // kernel on the stream drains; it runs its prologue (shared-memory / mbarrier setup,
 // index math) and then blocks in griddepcontrol.wait until the previous grid has completed
