@@ -3,6 +3,14 @@
 #include "taco_launch.h"
 #include "taco_tile.cuh"
 
+#ifndef TACO_K2_REG_BF16_B256
+// bf16-output K2 at B = 256 on the register kernel: alone 17.3 vs 16.2 us (tile), but the
+// K1 -> K2 round trip (bench value) 3,454 vs 3,379 GB/s -- the register K2 follows the register
+// K1 with the same CTA shape under PDL and reads K1's L2-resident messages.  fp32 output (the
+// reference's path, and K3's decode) stays on the tile kernel.
+#define TACO_K2_REG_BF16_B256 1
+#endif
+
 namespace taco_impl {
 using namespace taco_dev;
 
@@ -13,7 +21,8 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
         // measured (profiles/README.md): tile kernels for B >= 256 and fp32 output at
         // B = 128; the register kernel (K2_EMAX lanes geometry) at B = 64 and bf16 B = 128
-        const bool tile = B >= 256 || (B == 128 && std::is_same<T, float>::value);
+        const bool tile = (B >= 256 && !(TACO_K2_REG_BF16_B256 && B == 256 && std::is_same<T, __nv_bfloat16>::value)) ||
+                          (B == 128 && std::is_same<T, float>::value);
         if (kernel_family() != 2 && (tile || kernel_family() == 1)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K2T<NB, T>;

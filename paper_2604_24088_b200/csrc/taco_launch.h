@@ -82,9 +82,13 @@ cudaError_t launch_peer_barrier(const PeerSlots& f, uint32_t rank, uint32_t P, u
 #ifndef TACO_K2_EMAX_B1024
 #define TACO_K2_EMAX_B1024 TACO_K2_EMAX
 #endif
+#ifndef TACO_K2_EMAX_B256
+#define TACO_K2_EMAX_B256 TACO_K2_EMAX  // the register decode at B = 256 (family "reg" only)
+#endif
 template <int B>
 constexpr int k2_emax() {
-    return B == 2048 ? 64 : B == 64 ? TACO_K2_EMAX_B64 : B == 1024 ? TACO_K2_EMAX_B1024 : TACO_K2_EMAX;
+    return B == 2048 ? 64 : B == 64 ? TACO_K2_EMAX_B64 : B == 1024 ? TACO_K2_EMAX_B1024 : B == 256 ? TACO_K2_EMAX_B256
+                                                                                         : TACO_K2_EMAX;
 }
 
 // Programmatic dependent launch (sm_90+): the kernel may be scheduled while the previous
