@@ -88,6 +88,46 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
             "gpu_launches_per_step": 5, "barriers_per_step": 2}
 
 
+def _sp_leg(args, n, cfg, xs, stream, use_graphs):
+    """CompressedReduceScatter of the [n] tensor and CompressedAllGather of its [n/P] slice,
+    timed like the all-reduce, next to dist.reduce_scatter_tensor / all_gather_into_tensor
+    bf16 on the same tensors."""
+    from . import collective
+
+    world = dist.get_world_size()
+    dev = xs[0].device
+    rs = collective.CompressedReduceScatter(n, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=dev)
+    S = rs.shard_len
+    ag = collective.CompressedAllGather(S, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=dev)
+    rs_out = torch.empty(S, dtype=torch.bfloat16, device=dev)
+    ag_in = xs[0][:S].clone()
+    ag_out = torch.empty(world * S, dtype=torch.bfloat16, device=dev)
+    if use_graphs:
+        g_rs, g_ag = collective.Graphed(rs, xs[0], rs_out), collective.Graphed(ag, ag_in, ag_out)
+        rs_step, ag_step = (lambda i: g_rs()), (lambda i: g_ag())
+    else:
+        rs_step, ag_step = (lambda i: rs(xs[0], rs_out)), (lambda i: ag(ag_in, ag_out))
+    nx = xs[0][: world * S] if xs[0].numel() >= world * S else torch.nn.functional.pad(xs[0], (0, world * S - n))
+    nrs = torch.empty(S, dtype=torch.bfloat16, device=dev)
+    nag = torch.empty(world * S, dtype=torch.bfloat16, device=dev)
+    rep = {}
+    for name, fn, ref_fn, byts in (
+            ("reduce_scatter", rs_step, lambda i: dist.reduce_scatter_tensor(nrs, nx), 2 * n),
+            ("all_gather", ag_step, lambda i: dist.all_gather_into_tensor(nag, ag_in), 2 * world * S)):
+        for i in range(args.warmup):
+            fn(i)
+        t = _timed(fn, args.steps, stream) / args.steps
+        for i in range(args.warmup):
+            ref_fn(i)
+        tn = _timed(ref_fn, args.steps, stream) / args.steps
+        rep[name] = {"ms_per_step": round(t, 5), "algbw_GBps": round(byts / (t * 1e-3) / 1e9, 1),
+                     "nccl_bf16_ms_per_step": round(tn, 5), "speedup_vs_nccl_bf16": round(tn / t, 3),
+                     "wire_bytes_per_rank": (rs if name == "reduce_scatter" else ag).wire_bytes_per_rank()}
+    rs.ar.codec.check()
+    ag.codec.check()
+    return rep
+
+
 def run_collective(args, rows, cols, clock_sampler, peaks):
     from . import _abi, collective
     from ._abi import make_config
@@ -169,6 +209,9 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     # memory (peer.py): no NCCL call on the data path; must be bit-identical to the above
     peer_rep = _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R)
 
+    # the sequence-parallel pair on the same tensors, vs NCCL bf16 reduce-scatter / all-gather
+    sp_rep = _sp_leg(args, n, cfg, xs, stream, graphs is not None)
+
     # e2e: pinned host tensor -> H2D -> compressed all-reduce -> D2H, every step
     xh = xs[0].cpu().pin_memory()
     yh = torch.empty(n, dtype=torch.bfloat16).pin_memory()
@@ -230,6 +273,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
                     "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n,
                     "api": "collective.TwoShotAllReduce (pinned host in / out)"},
             "peer_memory_twoshot": peer_rep,
+            "sequence_parallel": sp_rep,
             "ranks_agree": bool(abs(float(mx.item()) - float(mn.item())) == 0.0),
             "gpu_launches": 3 * len(ar.ch.ranges) * args.steps,
             "clocks": clk.summary(),

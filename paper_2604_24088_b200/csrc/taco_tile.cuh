@@ -765,7 +765,7 @@ __device__ __forceinline__ void xpose_read1(const float* xb, float2 (&w)[TG<NB>:
 }
 
 template <int NB, typename TAcc>
-__global__ void __launch_bounds__(kTileWarps * 32)
+__global__ void __launch_bounds__(kTileWarps * 32, NB <= 8 ? 4 : 2)
     k_reduce_encode_tile(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg, TAcc* __restrict__ acc_out,
                          ShardArgs a, CodecConsts c) {
     using Gm = TG<NB>;
@@ -830,12 +830,26 @@ __global__ void __launch_bounds__(kTileWarps * 32)
             else acc[rr / 2].x = 0.0f;
         }
     }
-    if (live && acc_out) {
-        TAcc* dst = acc_out + (a.blk0 + kk) * B;
+    if (acc_out) {  // the stage-1 sum (the SP reduce-scatter output)
+        if (__all_sync(kFull, tile_full<B, kBlocks>(a, 0, kk0))) {
+            // whole tile: staged through xb, coalesced 128-bit stores (as K2's output)
+            constexpr int EPC = 16 / (int)sizeof(TAcc);
+            __syncwarp();
+            unsigned char* ob = reinterpret_cast<unsigned char*>(xb);
+            stage_out<NB, TAcc>(ob, acc, g, q);
+            __syncwarp();
+            TAcc* dst = acc_out + (a.blk0 + kk0) * B;
 #pragma unroll
-        for (int rr = 0; rr < Gm::E; ++rr) {
-            const int pos = Gm::pos2(rr, q);
-            if (pos < valid) store_one(dst + pos, (rr & 1) ? acc[rr / 2].y : acc[rr / 2].x);
+            for (int j = lane; j < Gm::TILE / EPC; j += 32)
+                *reinterpret_cast<uint4*>(dst + (uint64_t)j * EPC) =
+                    *reinterpret_cast<const uint4*>(ob + 16 * swz((uint32_t)j));
+        } else if (live) {
+            TAcc* dst = acc_out + (a.blk0 + kk) * B;
+#pragma unroll
+            for (int rr = 0; rr < Gm::E; ++rr) {
+                const int pos = Gm::pos2(rr, q);
+                if (pos < valid) store_one(dst + pos, (rr & 1) ? acc[rr / 2].y : acc[rr / 2].x);
+            }
         }
     }
     if (out_msg == nullptr) {  // reduce-scatter: the fp32 sum is the product
