@@ -125,6 +125,46 @@ def _sp_leg(args, n, cfg, xs, stream, use_graphs):
                      "wire_bytes_per_rank": (rs if name == "reduce_scatter" else ag).wire_bytes_per_rank()}
     rs.ar.codec.check()
     ag.codec.check()
+    # the same pair over peer memory (peer.py), checked bit for bit against the NCCL transport
+    from . import peer
+    from ._abi import TacoError
+    try:
+        prs = peer.PeerReduceScatter(n, cfg, dtype=torch.bfloat16, device=dev, timeout_ms=20_000)
+        pag = peer.PeerAllGather(S, cfg, dtype=torch.bfloat16, device=dev, timeout_ms=20_000)
+    except TacoError as e:
+        rep["peer_memory"] = {"error": str(e)}
+        return rep
+    p_rs = torch.empty_like(rs_out)
+    p_ag = torch.empty_like(ag_out)
+    err = ""
+    try:
+        for i in range(args.warmup):
+            prs(xs[0], p_rs)
+            pag(ag_in, p_ag)
+        torch.cuda.synchronize()
+        prs.check()
+        pag.check()
+    except TacoError as e:
+        err = str(e)
+    t = torch.tensor([0 if err else 1], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    if int(t.item()) == 1:
+        t_rs = _timed(lambda i: prs(xs[0], p_rs), args.steps, stream) / args.steps
+        t_ag = _timed(lambda i: pag(ag_in, p_ag), args.steps, stream) / args.steps
+        rs(xs[0], rs_out)
+        ag(ag_in, ag_out)
+        prs(xs[0], p_rs)
+        pag(ag_in, p_ag)
+        torch.cuda.synchronize()
+        same = torch.tensor([int(torch.equal(rs_out.view(torch.int16), p_rs.view(torch.int16))
+                                 and torch.equal(ag_out.view(torch.int16), p_ag.view(torch.int16)))], device=dev)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        rep["peer_memory"] = {"reduce_scatter_ms_per_step": round(t_rs, 5), "all_gather_ms_per_step": round(t_ag, 5),
+                              "bit_identical_to_nccl_transport": bool(int(same.item()) == 1)}
+    else:
+        rep["peer_memory"] = {"error": err or "failed on another rank"}
+    prs.close()
+    pag.close()
     return rep
 
 
