@@ -3,6 +3,9 @@
 #include "taco_launch.h"
 #include "taco_tile.cuh"
 
+#ifndef TACO_K2_VMAX_B256
+#define TACO_K2_VMAX_B256 16  // codes per lane run of the register K2 at B = 256 (32: 22.3 vs 17.4 us)
+#endif
 #ifndef TACO_K2_REG_BF16_B256
 // bf16-output K2 at B = 256 on the register kernel: alone 17.3 vs 16.2 us (tile), but the
 // K1 -> K2 round trip (bench value) 3,454 vs 3,379 GB/s -- the register K2 follows the register
@@ -34,7 +37,7 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         }
     }
     if constexpr (B <= 1024 || (B == 2048 && FMT == 0)) {  // B = 2048: one warp per block
-        constexpr int VMAX = 16, EMAX = FMT == 0 ? k2_emax<B>() : 32;
+        constexpr int VMAX = B == 256 ? TACO_K2_VMAX_B256 : 16, EMAX = FMT == 0 ? k2_emax<B>() : 32;
         using Cf = K2Cfg<B, T, FMT, EMAX, VMAX>;
         const uint64_t tps = (a.nblk + Cf::Gm::G - 1) / Cf::Gm::G;
         auto* kern = &k_decompress<B, T, FMT, EMAX, VMAX>;
