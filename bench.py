@@ -195,6 +195,33 @@ def run_taco_single(args) -> dict:
     dominant = ("k1", k1_ms, k1_gbs, bpe["k1"]) if k1_ms >= k2_ms else ("k2", k2_ms, k2_gbs, bpe["k2"])
     traffic = ncu_traffic("compress" if dominant[0] == "k1" else "decompress")
 
+    # ---- configs[0] beside it: the reference's CPU-runnable case, [1024 x 768] fp32 round trip
+    # on one rank (L2-resident, 7.9 MB: reported in microseconds)
+    n0 = 1024 * 768
+    m0 = -(-n0 // args.block_size)
+    lay0 = _abi.msg_layout(cfg, m0)
+    x0 = torch.randn(n0, generator=g, device=dev)
+    msg0 = torch.empty((1, lay0.msg_stride), dtype=torch.uint8, device=dev)
+    y0 = torch.empty(n0, device=dev)
+
+    def rt0():
+        _abi.check(lib.taco_compress_dev(C.byref(cfg), C.c_void_p(x0.data_ptr()), _abi.DT_F32, n0, 1, 0, m0,
+                                         C.c_void_p(msg0.data_ptr()), lay0.msg_stride, flags.ptr(), sp))
+        _abi.check(lib.taco_decompress_dev(C.byref(cfg), C.c_void_p(msg0.data_ptr()), lay0.msg_stride, 1, n0, 0, m0,
+                                           C.c_void_p(y0.data_ptr()), _abi.DT_F32, flags.ptr(), sp))
+
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            rt0()
+        c0a, c0b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0a.record(stream)
+        for _ in range(args.steps):
+            rt0()
+        c0b.record(stream)
+        stream.synchronize()
+    flags.check()
+    cfg0_us = c0a.elapsed_time(c0b) / args.steps * 1e3
+
     # ---- e2e through the C-ABI host call (pinned host buffers, H2D + D2H inside the timed region)
     hc = codec.HostContext(0)
     xh = xs[0].cpu().pin_memory()
@@ -252,6 +279,8 @@ def run_taco_single(args) -> dict:
                 "api": "taco_roundtrip_host (C ABI, pinned host buffers)", "matches_device_path": bool(same)},
         "gpu_launches": 2 * args.steps,  # K1 + K2 per step inside the timed region
         "wall_s_timed_region": round(t_wall, 4),
+        "configs0": {"workload": "[1024 x 768] fp32 compress + decompress round trip, 1 rank (L2-resident)",
+                     "us_per_roundtrip": round(cfg0_us, 2), "launches_per_roundtrip": 2},
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline:
