@@ -392,7 +392,13 @@ def main():
     ap.add_argument("--chunks", type=int, default=2, help="N>1: pipelined chunks per shard")
     ap.add_argument("--eager", action="store_true", help="N>1: no CUDA-graph capture of the step")
     ap.add_argument("--collective", action="store_true", help="run the all-reduce leg even at world size 1")
+    ap.add_argument("--shape", type=str, default=None,
+                    help="ROWSxCOLS of the per-rank tensor (default configs[1] 8192x2560; e.g. configs[2] "
+                         "16384x3584, configs[3] 16384x5120)")
     args = ap.parse_args()
+    if args.shape:
+        global ROWS, COLS
+        ROWS, COLS = (int(v) for v in args.shape.lower().split("x"))
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
