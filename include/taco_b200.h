@@ -25,6 +25,10 @@
  * msg_bytes = scal_offset + 8*nblocks (== nblocks*(B+8) whenever B >= 16, i.e. the
  * reference's per-block wire cost, collective.cpp:50-58 minus the 22-byte archive
  * header); msg_stride = msg_bytes rounded up to 16.
+ * Alignment rule: the kernels move messages with 16-byte vector / TMA accesses, so every
+ * message buffer passed to the device API must be 16-byte aligned and, when it holds more
+ * than one message, its stride a multiple of 16 (use taco_layout.msg_stride); otherwise
+ * the call returns TACO_ERR_USAGE before any launch.
  */
 #ifndef TACO_B200_H
 #define TACO_B200_H
@@ -300,6 +304,14 @@ int taco_error_report_dev(const void* original, int orig_dtype, const void* reco
  * taco::fp8_encode / fp8_decode (fp8.hpp:28-34) for bulk checks on the device. */
 int taco_fp8_encode_dev(const float* x, uint64_t n, int format, uint8_t* out, void* stream);
 int taco_fp8_decode_dev(const uint8_t* codes, uint64_t n, int format, float* out, void* stream);
+
+/* ----------------------------------------------------------------- inputs ---------
+ * taco::generate (analysis.hpp:40; analysis.cpp:70-95, rng.cpp): the reference's synthetic
+ * tensors with identical values -- kind 0 = Gaussian N(0,1), 1 = near-zero mixture
+ * (dense_sigma body, tail_sigma tail of tail_fraction*n elements, shuffled).  Host
+ * routine (one sequential xoshiro256++ stream); fills out[0..n). */
+int taco_generate_host(int kind, uint64_t n, uint64_t seed, double dense_sigma, double tail_sigma,
+                       double tail_fraction, float* out);
 
 #ifdef __cplusplus
 }

@@ -132,6 +132,7 @@ _SIGNATURES = {
                                               _U64, _U64, _P, _I, _P, _P]),
     "taco_fp8_encode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
     "taco_fp8_decode_dev": (C.c_int, [_P, _U64, _I, _P, _P]),
+    "taco_generate_host": (C.c_int, [_I, _U64, _U64, C.c_double, C.c_double, C.c_double, _P]),
 }
 
 _lib = None

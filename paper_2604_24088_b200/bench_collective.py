@@ -14,6 +14,56 @@ import torch
 import torch.distributed as dist
 
 
+def reference_collective(args, world: int) -> dict:
+    """`bench.py --impl reference` at N > 1: the reference's own taco::allreduce(TwoShot)
+    (oracle/_ref, unmodified sources) simulating the `world` ranks in one host process
+    (collective.cpp:75-111) on the host cores -- rank 0 only.  Per-rank inputs are the
+    reference generator's mixture with seed 100 + r (acceptance.cpp:380).  A bounded sample
+    of each rank's tensor (the simulation runs all P ranks' codec calls serially in one
+    process: the full configs take 1-14 s per step)."""
+    import numpy as np
+    import torch
+
+    from oracle.oracle import Ref
+
+    cores = os.cpu_count() or 1
+    ref = Ref()
+    n_full = args.rows * args.cols
+    per_rank = min(n_full, 1 << 20)
+    ins = np.stack([torch.from_numpy(ref.generate(1, per_rank, 100 + r)).to(torch.bfloat16).float().numpy()
+                    for r in range(world)])
+    ref.set_threads(cores)
+    for _ in range(args.warmup):
+        ref.allreduce(ins, args.block_size)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ref.allreduce(ins, args.block_size)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = world * 2 * per_rank / dt / 1e9
+    desc = (f"taco::allreduce(TwoShot) simulating {world} ranks in one process, {per_rank} elements per rank "
+            f"(bounded sample of the {n_full}-element per-rank tensors), TACO_THREADS={cores}")
+    return {"impl": "reference", "metric": "taco_twoshot_allreduce_algbw_GBps", "value": round(value, 4),
+            "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16", "data": "synthetic: taco::generate near-zero mixture, seed 100 + rank",
+            "config": workload_config(args, world),
+            "cpu_baseline": {"value": round(value, 4), "unit": "GB/s", "cores": cores, "kind": "reference",
+                             "sample": desc},
+            "e2e": {"value": round(value, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+
+
+def workload_config(args, world: int) -> dict:
+    """The N > 1 workload that `--gpus N` names (identical in both arms)."""
+    idx = getattr(args, "config", None)
+    what = {1: "row-parallel output all-reduce", 2: "sequence-parallel reduce-scatter + all-gather",
+            3: "forward activation + backward activation-gradient all-reduce"}.get(idx, "all-reduce")
+    return {"workload": f"configs[{idx}] per-rank tensor [{args.rows} x {args.cols}] bf16, TP={world} FP8 two-shot "
+                        f"{what}" if idx is not None else f"[{args.rows} x {args.cols}] bf16, TP={world} two-shot",
+            "shape": [args.rows, args.cols], "elements_per_rank": args.rows * args.cols,
+            "block_size": args.block_size, "format": "E4M3", "parallelism": f"tp{world}"}
+
+
 def _timed(fn, steps, stream):
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     dist.barrier()

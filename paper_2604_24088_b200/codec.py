@@ -49,6 +49,33 @@ def cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
+def _require_buffer(t: torch.Tensor, what: str, min_numel: int, dtype=None, device=None) -> None:
+    """Caller-supplied buffers are forwarded to the kernels as raw pointers: check that they
+    are dense, large enough, of the right dtype and on the right device before any launch
+    (an undersized buffer would otherwise be an out-of-bounds device access)."""
+    if not t.is_contiguous():
+        raise TacoError(_abi.ERR_USAGE, f"{what} must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TacoError(_abi.ERR_USAGE, f"{what} must be {dtype}, got {t.dtype}")
+    if device is not None and t.device != device:
+        raise TacoError(_abi.ERR_USAGE, f"{what} must live on {device}, got {t.device}")
+    if t.numel() < min_numel:
+        raise TacoError(_abi.ERR_USAGE, f"{what} holds {t.numel()} elements, needs {min_numel}")
+
+
+def generate(kind: int, n: int, seed: int, dense_sigma: float = 1e-3, tail_sigma: float = 1.0,
+             tail_fraction: float = 0.01) -> torch.Tensor:
+    """taco::generate (analysis.hpp:40): the reference's synthetic tensor, value for value
+    (kind 0 Gaussian, 1 near-zero mixture), as a CPU float32 tensor (SURVEY §8d inputs)."""
+    out = torch.empty(int(n), dtype=torch.float32)
+    _abi.check(_abi.lib().taco_generate_host(int(kind), int(n), int(seed), float(dense_sigma), float(tail_sigma),
+                                             float(tail_fraction), _ptr(out)))
+    return out
+
+
+GAUSSIAN, NEAR_ZERO_MIXTURE = 0, 1
+
+
 @dataclass
 class Geometry:
     """Shard / block / message geometry of one call (collective.cpp:76-87)."""
@@ -101,6 +128,7 @@ def compress(x: torch.Tensor, cfg: Config, shards: int = 1, blk: tuple[int, int]
     if out is None:
         out = torch.empty((shards, lay.msg_stride), dtype=torch.uint8, device=x.device)
     _require_cuda(out)
+    _require_buffer(out, "compress out", (shards - 1) * lay.msg_stride + lay.msg_bytes, torch.uint8, x.device)
     _abi.check(_abi.lib().taco_compress_dev(C.byref(cfg), _ptr(x), _dtype_code(x.dtype), n, shards, b0, b1,
                                             _ptr(out), lay.msg_stride, flags.ptr() if flags else None,
                                             C.c_void_p(_stream(stream))))
@@ -114,10 +142,17 @@ def decompress(msgs: torch.Tensor, n: int, cfg: Config, shards: int = 1, out_dty
     _require_cuda(msgs)
     g = Geometry(n, shards, cfg.block_size)
     b0, b1 = blk if blk is not None else (0, g.blocks if n else 0)
-    stride = msg_stride if msg_stride is not None else _abi.msg_layout(cfg, b1 - b0).msg_stride
+    lay = _abi.msg_layout(cfg, b1 - b0)
+    stride = msg_stride if msg_stride is not None else lay.msg_stride
+    if not msgs.is_contiguous() or msgs.dtype != torch.uint8:
+        raise TacoError(_abi.ERR_USAGE, "messages must be a contiguous uint8 tensor")
+    if msgs.numel() < (shards - 1) * stride + lay.msg_bytes:
+        # codec.cpp:272-273: the message holds fewer blocks than the declared length needs
+        raise TacoError(_abi.ERR_CORRUPT, "block count does not match the declared length")
     if out is None:
         out = torch.empty(n, dtype=out_dtype, device=msgs.device)
     _require_cuda(out)
+    _require_buffer(out, "decompress out", n, device=msgs.device)
     _abi.check(_abi.lib().taco_decompress_dev(C.byref(cfg), _ptr(msgs), stride, shards, n, b0, b1, _ptr(out),
                                               _dtype_code(out.dtype), flags.ptr() if flags else None,
                                               C.c_void_p(_stream(stream))))
@@ -133,6 +168,12 @@ def reduce_encode(msgs: torch.Tensor, nranks: int, shard_len: int, cfg: Config, 
     _require_cuda(msgs, out_msg, acc_out)
     m = cdiv(shard_len, cfg.block_size)
     b0, b1 = blk if blk is not None else (0, m)
+    lay = _abi.msg_layout(cfg, b1 - b0)
+    _require_buffer(msgs, "reduce_encode messages", (nranks - 1) * rank_stride + lay.msg_bytes, torch.uint8)
+    if out_msg is not None:
+        _require_buffer(out_msg, "reduce_encode out_msg", lay.msg_bytes, torch.uint8, msgs.device)
+    if acc_out is not None:
+        _require_buffer(acc_out, "reduce_encode acc_out", min(shard_len, b1 * cfg.block_size), device=msgs.device)
     _abi.check(_abi.lib().taco_reduce_encode_dev(
         C.byref(cfg), _ptr(msgs), rank_stride, nranks, shard_len, b0, b1, _ptr(out_msg), _ptr(acc_out),
         _dtype_code(acc_out.dtype) if acc_out is not None else DT_F32, flags.ptr() if flags else None,
@@ -263,13 +304,25 @@ class HostContext:
         except Exception:
             pass
 
+    @staticmethod
+    def _host(t: torch.Tensor, what: str, numel: int | None = None) -> None:
+        if t.is_cuda:
+            raise TacoError(_abi.ERR_USAGE, f"{what} must be a host (CPU) tensor")
+        if not t.is_contiguous():
+            raise TacoError(_abi.ERR_USAGE, f"{what} must be contiguous")
+        if numel is not None and t.numel() != numel:
+            raise TacoError(_abi.ERR_USAGE, f"{what} holds {t.numel()} elements, expected {numel}")
+
     def roundtrip(self, x: torch.Tensor, cfg: Config, out: torch.Tensor) -> torch.Tensor:
         """compress -> decompress of a host tensor; out is a host tensor of x's size."""
+        self._host(x, "roundtrip input")
+        self._host(out, "roundtrip out", x.numel())
         _abi.check(_abi.lib().taco_roundtrip_host(self.h, C.byref(cfg), _ptr(x), _dtype_code(x.dtype), x.numel(),
                                                   _ptr(out), _dtype_code(out.dtype)))
         return out
 
     def compress(self, x: torch.Tensor, cfg: Config) -> torch.Tensor:
+        self._host(x, "compress input")
         m = cdiv(x.numel(), cfg.block_size)
         msg = torch.empty(_abi.msg_layout(cfg, m).msg_bytes, dtype=torch.uint8)
         _abi.check(_abi.lib().taco_compress_host(self.h, C.byref(cfg), _ptr(x), _dtype_code(x.dtype), x.numel(),
@@ -277,12 +330,18 @@ class HostContext:
         return msg
 
     def decompress(self, msg: torch.Tensor, n: int, cfg: Config, out_dtype=torch.float32) -> torch.Tensor:
+        self._host(msg, "compressed message")
+        if msg.dtype != torch.uint8 or msg.numel() < _abi.msg_layout(cfg, cdiv(n, cfg.block_size)).msg_bytes:
+            raise TacoError(_abi.ERR_CORRUPT, "block count does not match the declared length")
         out = torch.empty(n, dtype=out_dtype)
         _abi.check(_abi.lib().taco_decompress_host(self.h, C.byref(cfg), _ptr(msg), n, _ptr(out),
                                                    _dtype_code(out_dtype)))
         return out
 
     def allreduce_sim(self, inputs: torch.Tensor, cfg: Config, want_stage1: bool = False):
+        self._host(inputs, "rank inputs")
+        if inputs.dtype != torch.float32:
+            raise TacoError(_abi.ERR_USAGE, "rank inputs must be float32 (taco::RankSet)")
         p, n = inputs.shape
         res = torch.empty(n, dtype=torch.float32)
         st = torch.empty(p * cdiv(n, p), dtype=torch.float32) if want_stage1 else None

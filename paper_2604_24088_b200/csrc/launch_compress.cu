@@ -2,7 +2,6 @@
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
 #include "taco_tile.cuh"
-#include "taco_r2.cuh"
 #include "taco_tc.cuh"
 
 #include <cudaTypedefs.h>
@@ -93,20 +92,6 @@ cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
         if (kernel_family() == 5 && a.ndst == 0) {
             const cudaError_t e = run_tc(l, a, c);
             if (e != cudaErrorNotSupported) return e;
-        }
-    }
-    if constexpr (FMT == 0 && B >= 32 && B <= 1024) {
-        if (kernel_family() == 3 && a.ndst == 0) {
-            using Cf = r2::Cfg<B, T>;
-            const uint64_t tps = (a.nblk + Cf::G - 1) / Cf::G;
-            auto* kern = &r2::k_compress_r2<B, T>;
-            const unsigned grid = persistent_grid(kern, r2::kWarps * 32, Cf::SMEM, tps * a.P, r2::kWarps);
-            uint32_t* ctr = claim_counter();
-            if (!ctr) return cudaErrorMemoryAllocation;
-            kern<<<grid, r2::kWarps * 32, Cf::SMEM, l.stream>>>(static_cast<const T*>(l.in),
-                                                               static_cast<uint8_t*>(l.out), a, c,
-                                                               make_fastdiv((uint32_t)tps), ctr);
-            return cudaGetLastError();
         }
     }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {

@@ -109,6 +109,14 @@ taco_layout layout_of(uint64_t pb, uint64_t nblocks) {  // pb = payload bytes pe
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// Messages are read and written with 16-byte vector / TMA accesses: every message base must
+// be 16-byte aligned, i.e. the buffer and (with more than one message) the stride.
+int check_msg_buffer(const void* p, uint64_t stride, uint64_t count, const char* what) {
+    if (!aligned16(p) || (count > 1 && stride % 16 != 0))
+        return fail(TACO_ERR_USAGE, std::string(what) + " must be 16-byte aligned (buffer and stride)");
+    return TACO_OK;
+}
+
 int check_range(uint64_t m, uint64_t blk_begin, uint64_t blk_end) {
     if (blk_begin > blk_end || blk_end > m)
         return fail(TACO_ERR_USAGE, "block range exceeds the shard's block count");
@@ -144,7 +152,6 @@ int kernel_family() {
         const char* v = std::getenv("TACO_B200_KERNELS");
         if (v && std::strcmp(v, "reg") == 0) return 2;
         if (v && std::strcmp(v, "tile") == 0) return 1;
-        if (v && std::strcmp(v, "r2") == 0) return 3;
         if (v && std::strcmp(v, "tc") == 0) return 5;
         return 0;
     }();
@@ -208,6 +215,8 @@ extern "C" {
 
 int taco_abi_version(void) { return TACO_B200_ABI_VERSION; }
 
+int taco_set_error(int code, const char* msg) { return fail(code, msg); }
+
 const char* taco_last_error(void) { return g_err.c_str(); }
 
 taco_config taco_default_config(void) {
@@ -260,6 +269,7 @@ int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
     const taco_layout lay = layout_of(payload_of(cfg), blk_end - blk_begin);
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if (int rc = check_msg_buffer(msgs, msg_stride, shards, "messages")) return rc;
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(x) && (shards == 1 || S % 8 == 0), d_flags};
     taco_dev::with_full_blocks(a, b);
@@ -286,6 +296,7 @@ int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_s
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
     const taco_layout lay = layout_of(payload_of(cfg), blk_end - blk_begin);
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if (int rc = check_msg_buffer(msgs, msg_stride, shards, "messages")) return rc;
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
                 aligned16(out) && (shards == 1 || S % 8 == 0), d_flags};
     taco_dev::with_full_blocks(a, b);
@@ -315,6 +326,9 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     if (int rc = check_range(m, blk_begin, blk_end)) return rc;
     const taco_layout lay = layout_of(b, blk_end - blk_begin);
     if (nranks > 1 && rank_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if (int rc = check_msg_buffer(msgs, rank_stride, nranks, "messages")) return rc;
+    if (out_msg)
+        if (int rc = check_msg_buffer(out_msg, 0, 1, "out_msg")) return rc;
     ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
                 acc_out ? aligned16(acc_out) : 0, d_flags};
     taco_dev::with_full_blocks(a, b);
@@ -484,8 +498,12 @@ int taco_reduce_encode_ptrs_dev(const taco_config* cfg, const void* const* msgs,
                                 int acc_dtype, int* d_flags, void* stream) {
     if (!msgs) return fail(TACO_ERR_USAGE, "null message pointer array");
     if (nranks == 0 || nranks > TACO_MAX_PEERS) return fail(TACO_ERR_USAGE, "pointer-array reduction takes 1 to 8 ranks");
-    for (uint32_t r = 0; r < nranks; ++r)
+    for (uint32_t r = 0; r < nranks; ++r) {
         if (!msgs[r]) return fail(TACO_ERR_USAGE, "null message pointer");
+        if (int rc = check_msg_buffer(msgs[r], 0, 1, "messages")) return rc;
+    }
+    if (out_msg)
+        if (int rc = check_msg_buffer(out_msg, 0, 1, "out_msg")) return rc;
     if (int rc = check_config(cfg)) return rc;
     if (acc_out)
         if (int rc = check_dtype(acc_dtype)) return rc;

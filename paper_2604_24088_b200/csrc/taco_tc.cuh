@@ -33,7 +33,6 @@
 #include <cuda.h>
 
 #include "taco_kernels.cuh"
-#include "taco_r2.cuh"
 
 #ifndef TACO_TC_DEBUG
 #define TACO_TC_DEBUG 0
@@ -199,8 +198,8 @@ __device__ __forceinline__ double slab_sumsq(const unsigned char* slab, int r) {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
 #if TACO_SUMSQ == 1
-            facc[(2 * i) & 7] = r2::fma_bf16(w[i] & 0xffffu, facc[(2 * i) & 7]);
-            facc[(2 * i + 1) & 7] = r2::fma_bf16(w[i] >> 16, facc[(2 * i + 1) & 7]);
+            facc[(2 * i) & 7] = fma_bf16_sq(w[i] & 0xffffu, facc[(2 * i) & 7]);
+            facc[(2 * i + 1) & 7] = fma_bf16_sq(w[i] >> 16, facc[(2 * i + 1) & 7]);
 #else
             const double d0 = tile::bf16_to_f64(w[i] & 0xffffu), d1 = tile::bf16_to_f64(w[i] >> 16);
             acc[(2 * i) & 3] = fma(d0, d0, acc[(2 * i) & 3]);
@@ -368,7 +367,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
             __syncwarp();
             if (lane == 0) mbar_arrive_u(bar_empty + 8 * s);
-            const float alpha = r2::alpha_of(ss, c);
+            const float alpha = block_alpha_fast(ss, c);
             mbar_wait_u(bar_ssempty + 8 * par, ((i >> 1) & 1) ^ 1);
             ss_buf[par * kM + r] = ss;
             al_buf[par * kM + r] = alpha;
@@ -431,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool overflow = !isfinite(ymax) && isfinite(ss);
             float s_blk;
             double k;
-            r2::scale_of((double)ymax, alpha, 1.0f, c, s_blk, k);
+            block_scale_fast((double)ymax, alpha, 1.0f, c, s_blk, k);
             const bool kfast = fabs(k) < 0x1p126 && (k == 0.0 || fabs(k) >= 0x1p-126);
             const float2 kk2 = make_float2((float)k, (float)k);
             uint32_t code[4][8];  // [q][word]: codes of outputs 64q + 32h .. +31

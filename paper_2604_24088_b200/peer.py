@@ -167,6 +167,27 @@ class _Mapped:
         self.region.free()
 
 
+def _input(x: torch.Tensor, n: int, device) -> torch.Tensor:
+    """The kernels read x through a raw pointer: make it a dense 1-D tensor on this
+    transport's device (a strided view such as buf[::2] would otherwise be read as if dense,
+    unlike the NCCL transport, which also goes through .contiguous())."""
+    if x.device != device:
+        raise TacoError(_abi.ERR_USAGE, f"input must live on {device}, got {x.device}")
+    x = x.reshape(-1).contiguous()
+    if x.numel() != n:
+        raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
+    return x
+
+
+def _output(out: torch.Tensor | None, numel: int, dtype, device) -> torch.Tensor:
+    if out is None:
+        return torch.empty(numel, dtype=dtype, device=device)
+    if not out.is_contiguous() or out.numel() != numel or out.device != device:
+        raise TacoError(_abi.ERR_USAGE, f"out must be a contiguous tensor of {numel} elements on {device}")
+    _dtype_code(out.dtype)
+    return out
+
+
 def _device(device):
     return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
 
@@ -198,11 +219,8 @@ class PeerTwoShotAllReduce:
         return 2 * (self.P - 1) * self.geo.lay.msg_bytes
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
-        x = x.reshape(-1)
-        if x.numel() != self.n:
-            raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
-        if out is None:
-            out = torch.empty(self.n, dtype=self.out_dtype, device=self.device)
+        x = _input(x, self.n, self.device)
+        out = _output(out, self.n, self.out_dtype, self.device)
         push_step(self.cfg, x, self.n, self.geo, self.peers, out, self.flags, self.timeout_ms)
         return out
 
@@ -239,11 +257,8 @@ class PeerReduceScatter:
         return (self.P - 1) * self.geo.lay.msg_bytes
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        x = x.reshape(-1)
-        if x.numel() != self.n:
-            raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
-        if out is None:
-            out = torch.empty(self.geo.S, dtype=self.out_dtype, device=self.device)
+        x = _input(x, self.n, self.device)
+        out = _output(out, self.geo.S, self.out_dtype, self.device)
         g, ps, lib = self.geo, self.map.peers, _abi.lib()
         st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
         _abi.check(lib.taco_compress_push_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n, C.byref(ps),
@@ -285,12 +300,9 @@ class PeerAllGather:
         return (self.P - 1) * self.lay.msg_bytes
 
     def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-        x = x.reshape(-1)
-        if x.numel() != self.n_local:
-            raise TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
+        x = _input(x, self.n_local, self.device)
         n = self.P * self.n_local
-        if out is None:
-            out = torch.empty(n, dtype=self.out_dtype, device=self.device)
+        out = _output(out, n, self.out_dtype, self.device)
         ps, lib = self.map.peers, _abi.lib()
         st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
         _abi.check(lib.taco_compress_bcast_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n_local,

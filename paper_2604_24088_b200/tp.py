@@ -14,7 +14,8 @@ FP8 two-shot collectives of ``collective.py`` into autograd with the usual regio
 plus ``RowParallelLinear`` / ``ColumnParallelLinear`` modules and ``torch.library`` custom
 ops (``taco_b200::compress`` / ``decompress``) so the codec is an opaque op under
 ``torch.compile`` / FX.  The collective objects (buffers, chunking, optional CUDA graphs)
-are cached per (group, size, dtype); the codec is injectable like in ``collective.py``.
+live in a bounded per-context LRU keyed on (group, size, dtype) and are released by
+``TpContext.close()``; the codec is injectable like in ``collective.py``.
 """
 from __future__ import annotations
 
@@ -24,27 +25,24 @@ import torch.distributed as dist
 from . import _abi, collective
 from ._abi import Config
 
-_CACHE: dict = {}
+from collections import OrderedDict
+
+# Collective objects own device buffers (and, for the peer transport, a CUDA-IPC region
+# mapped by every rank), so each TpContext keeps a bounded LRU of them keyed on the group
+# OBJECT (held by the key, so a collected group's id() cannot be reused for a stale entry).
+# Evicting or closing is collective for the peer transport: every rank makes the same calls
+# in the same order (SPMD), so they evict the same entries together.
+_MAX_CACHED = 8
 
 
-def _key(kind, group, n, dtype, cfg: Config, chunks):
-    return (kind, id(group), n, dtype, cfg.block_size, cfg.format, cfg.kind, chunks)
+def _key(kind, group, n, dtype, cfg: Config, chunks, codec, transport):
+    return (kind, group, n, dtype, cfg.block_size, cfg.format, cfg.kind, chunks, id(codec), transport)
 
 
-def _get(kind, group, n, dtype, cfg, chunks, device, codec, transport="nccl"):
-    k = _key(kind, group, n, dtype, cfg, chunks) + (id(codec), transport)
-    op = _CACHE.get(k)
-    if op is None:
-        if transport == "peer":  # exchange inside the kernels (peer.py)
-            from . import peer
-            cls = {"ar": peer.PeerTwoShotAllReduce, "rs": peer.PeerReduceScatter, "ag": peer.PeerAllGather}[kind]
-            op = cls(n, cfg, group, dtype=dtype, device=device)
-        else:
-            cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
-                   "ag": collective.CompressedAllGather}[kind]
-            op = cls(n, cfg, group, dtype=dtype, chunks=chunks, device=device, codec=codec)
-        _CACHE[k] = op
-    return op
+def _close(op) -> None:
+    close = getattr(op, "close", None)
+    if close is not None:
+        close()
 
 
 class TpContext:
@@ -63,13 +61,38 @@ class TpContext:
         self.chunks = chunks
         self.codec = codec
         self.transport = transport
+        self._ops: OrderedDict = OrderedDict()
+
+    def _get(self, kind, n, dtype, device):
+        k = _key(kind, self.group, n, dtype, self.cfg, self.chunks, self.codec, self.transport)
+        op = self._ops.get(k)
+        if op is not None:
+            self._ops.move_to_end(k)
+            return op
+        if self.transport == "peer":  # exchange inside the kernels (peer.py)
+            from . import peer
+            cls = {"ar": peer.PeerTwoShotAllReduce, "rs": peer.PeerReduceScatter, "ag": peer.PeerAllGather}[kind]
+            op = cls(n, self.cfg, self.group, dtype=dtype, device=device)
+        else:
+            cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
+                   "ag": collective.CompressedAllGather}[kind]
+            op = cls(n, self.cfg, self.group, dtype=dtype, chunks=self.chunks, device=device, codec=self.codec)
+        self._ops[k] = op
+        while len(self._ops) > _MAX_CACHED:
+            _close(self._ops.popitem(last=False)[1])
+        return op
+
+    def close(self) -> None:
+        """Release every cached collective (collective call for the peer transport)."""
+        while self._ops:
+            _close(self._ops.popitem(last=False)[1])
 
     @property
     def world(self) -> int:
         return dist.get_world_size(self.group)
 
     def all_reduce(self, x: torch.Tensor) -> torch.Tensor:
-        op = _get("ar", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
+        op = self._get("ar", x.numel(), x.dtype, x.device)
         return op(x.contiguous()).view(x.shape)
 
     def reduce_scatter(self, x: torch.Tensor) -> torch.Tensor:
@@ -77,12 +100,12 @@ class TpContext:
         w = self.world
         if x.shape[0] % w:
             raise _abi.TacoError(_abi.ERR_USAGE, "sequence length must divide by the tensor-parallel size")
-        op = _get("rs", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
+        op = self._get("rs", x.numel(), x.dtype, x.device)
         return op(x.contiguous()).view(x.shape[0] // w, *x.shape[1:])
 
     def all_gather(self, x: torch.Tensor) -> torch.Tensor:
         """x: this rank's token slice [t, ...] -> [world * t, ...]"""
-        op = _get("ag", self.group, x.numel(), x.dtype, self.cfg, self.chunks, x.device, self.codec, self.transport)
+        op = self._get("ag", x.numel(), x.dtype, x.device)
         return op(x.contiguous()).view(self.world * x.shape[0], *x.shape[1:])
 
 

@@ -134,3 +134,25 @@ def test_peer_abi_argument_checks_without_a_gpu():
     assert lib.taco_peer_barrier_dev(C.byref(ps), 8, 10, None, None) == _abi.ERR_USAGE
     assert lib.taco_flags_status(_abi.FLAG_PEER_TIMEOUT) == _abi.ERR_CUDA
     assert lib.taco_last_error().decode() == "peer barrier timed out"
+
+
+@pytest.mark.parametrize("kind,n,seed", [(0, 100_003, 7), (1, 100_003, 7), (1, 262_144, 101), (1, 1, 3)])
+def test_generate_matches_reference(kind, n, seed, ref):
+    # taco::generate (analysis.cpp:70-95) value for value: the bench's inputs are the
+    # reference's synthetic tensors
+    import numpy as np
+
+    from paper_2604_24088_b200 import codec
+    got = codec.generate(kind, n, seed).numpy()
+    want = ref.generate(kind, n, seed)
+    assert got.dtype == np.float32 and np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_generate_errors_match_reference():
+    from paper_2604_24088_b200 import codec
+    with pytest.raises(TacoError, match="synthetic tensor length must be positive"):
+        codec.generate(1, 0, 7)
+    with pytest.raises(TacoError, match=r"tail fraction must be in \[0, 1\]"):
+        codec.generate(1, 10, 7, tail_fraction=1.5)
+    with pytest.raises(TacoError, match="mixture sigmas must be positive"):
+        codec.generate(1, 10, 7, dense_sigma=0.0)

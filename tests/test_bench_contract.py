@@ -27,13 +27,26 @@ def _check(line, n):
 
 
 def test_reference_arm_n1():
-    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1"],
-                       cwd=ROOT, capture_output=True, text=True, timeout=300)
+    # configs[1]'s tensor keeps the CPU run short; the default is configs[3]
+    r = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1", "--warmup", "1",
+                        "--config", "1"], cwd=ROOT, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [x for x in r.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1
     d = _check(lines[0], 1)
     assert d["metric"] == "taco_compress_decompress_hbm_GBps"
+    assert d["config"]["shape"] == [8192, 2560] and "configs[1]" in d["config"]["workload"]
+
+
+def test_config_dict_is_shared_by_both_arms():
+    # the driver compares `config` between the arms: both build it from config_dict
+    sys.path.insert(0, ROOT)
+    import bench
+    a = bench.config_dict(3, 16384, 5120, 256, "x")
+    assert a["shape"] == [16384, 5120] and "configs[3]" in a["workload"] and a["in_dtype"] == "bf16"
+    assert bench.parse_shape("16384x3584") == (16384, 3584)
+    with pytest.raises(SystemExit):
+        bench.parse_shape("16384by3584")
 
 
 def test_reference_arm_torchrun_rank0_only():
