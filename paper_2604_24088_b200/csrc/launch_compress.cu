@@ -2,6 +2,7 @@
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
 #include "taco_tile.cuh"
+#include "taco_xk.cuh"
 #include "taco_tc.cuh"
 
 #include <cudaTypedefs.h>
@@ -85,17 +86,31 @@ cudaError_t run_tc(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     return cudaGetLastError();
 }
 
+// exchange-butterfly K1 (taco_xk.cuh): E4M3, 64 <= B <= 512
+template <int L, typename T>
+cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    using K = xk::K1X<L, T>;
+    const uint64_t tps = (a.nblk + K::G - 1) / K::G;
+    auto* kern = a.ndst ? &xk::k1x<L, T, true> : &xk::k1x<L, T, false>;
+    const unsigned grid = persistent_grid(kern, xk::kWarps * 32, K::SMEM, tps * a.P, xk::kWarps);
+    return launch_k(kern, grid, xk::kWarps * 32, K::SMEM, l.stream, static_cast<const T*>(l.in),
+                    static_cast<uint8_t*>(l.out), a, c, make_fastdiv((uint32_t)tps));
+}
+
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+        if (xk_family()) return run_xk<B / 64, T>(l, a, c);
+    }
     if constexpr (FMT == 0 && B == 256 && std::is_same<T, __nv_bfloat16>::value) {
-        if (kernel_family() == 5 && a.ndst == 0) {
+        if (legacy_family() == 5 && a.ndst == 0) {
             const cudaError_t e = run_tc(l, a, c);
             if (e != cudaErrorNotSupported) return e;
         }
     }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
-        const int fam = kernel_family();
+        const int fam = legacy_family();
         // fp32 input: the tile kernel for 128 <= B <= 512; at B = 64 the register kernel
         // (31.8 vs 41.3 us, profiles/README.md)
         if (fam == 1 || (fam == 0 && std::is_same<T, float>::value && B >= 128)) {

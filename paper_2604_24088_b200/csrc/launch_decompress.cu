@@ -2,6 +2,7 @@
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
 #include "taco_tile.cuh"
+#include "taco_xk.cuh"
 
 #ifndef TACO_K2_VMAX_B256
 #define TACO_K2_VMAX_B256 16  // codes per lane run of the register K2 at B = 256 (32: 22.3 vs 17.4 us)
@@ -18,15 +19,28 @@ namespace taco_impl {
 using namespace taco_dev;
 
 namespace {
+template <int L, typename T>
+cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    using K = xk::K2X<L>;
+    const uint64_t tps = (a.nblk + K::G - 1) / K::G;
+    auto* kern = &xk::k2x<L, T>;
+    const unsigned grid = persistent_grid(kern, xk::kWarps * 32, K::SMEM, tps * a.P, xk::kWarps);
+    return launch_k(kern, grid, xk::kWarps * 32, K::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
+                    static_cast<T*>(l.out), a, c, make_fastdiv((uint32_t)tps));
+}
+
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+        if (xk_family()) return run_xk<B / 64, T>(l, a, c);
+    }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
         // measured (profiles/README.md): tile kernels for B >= 256 and fp32 output at
         // B = 128; the register kernel (K2_EMAX lanes geometry) at B = 64 and bf16 B = 128
         const bool tile = (B >= 256 && !(TACO_K2_REG_BF16_B256 && B == 256 && std::is_same<T, __nv_bfloat16>::value)) ||
                           (B == 128 && std::is_same<T, float>::value);
-        if (kernel_family() != 2 && (tile || kernel_family() == 1)) {
+        if (legacy_family() != 2 && (tile || legacy_family() == 1)) {
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K2T<NB, T>;
             const uint64_t tps = (a.nblk + Cf::KB - 1) / Cf::KB;

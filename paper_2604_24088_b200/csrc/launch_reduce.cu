@@ -2,16 +2,30 @@
 #include "taco_kernels.cuh"
 #include "taco_launch.h"
 #include "taco_tile.cuh"
+#include "taco_xk.cuh"
 
 namespace taco_impl {
 using namespace taco_dev;
 
 namespace {
+template <int L, typename T>
+cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
+    using K = xk::K3X<L>;
+    auto* kern = &xk::k3x<L, T>;
+    const uint64_t tiles = (a.nblk + K::G - 1) / K::G;
+    const unsigned grid = (unsigned)((tiles + xk::kWarps - 1) / xk::kWarps);
+    return launch_k(kern, grid, xk::kWarps * 32, K::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
+                    static_cast<uint8_t*>(l.out), static_cast<T*>(l.acc), a, c);
+}
+
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0) return cudaSuccess;
+    if constexpr (FMT == 0 && B >= 64 && B <= 512) {
+        if (xk_family()) return run_xk<B / 64, T>(l, a, c);
+    }
     if constexpr (FMT == 0 && B >= 256 && B <= 512) {
-        if (kernel_family() != 2) {  // K2's decode is the tile kernel: decode with the same code
+        if (legacy_family() != 2) {  // K2's decode is the tile kernel: decode with the same code
             constexpr int NB = B == 64 ? 6 : B == 128 ? 7 : B == 256 ? 8 : 9;
             using Cf = tile::K3T<NB>;
             auto* kern = &tile::k_reduce_encode_tile<NB, T>;

@@ -153,6 +153,7 @@ int kernel_family() {
         if (v && std::strcmp(v, "reg") == 0) return 2;
         if (v && std::strcmp(v, "tile") == 0) return 1;
         if (v && std::strcmp(v, "tc") == 0) return 5;
+        if (v && std::strcmp(v, "r1") == 0) return 6;
         return 0;
     }();
     return fam;

@@ -40,7 +40,13 @@ inline unsigned persistent_grid(K kernel, int threads, size_t smem, uint64_t til
 // input (64 <= B <= 512), K2/K3 tile kernels.  5 = "tc": K1 on the tensor cores for bf16,
 // B = 256 (taco_tc.cuh; parity-exact, slower today).  1 = "tile" (K1 tile for bf16 too),
 // 2 = "reg" (the register kernels everywhere), 3 = "r2" (K1 r2).
+// 6 = "r1": round 1's default dispatch (the register / tile kernels below instead of the
+// exchange-butterfly family of taco_xk.cuh, which is the default for E4M3 at 64 <= B <= 512).
 int kernel_family();
+// the family the register / tile / tc dispatch sees ("r1" = its default)
+inline int legacy_family() { const int f = kernel_family(); return f == 6 ? 0 : f; }
+// whether E4M3 at 64 <= B <= 512 runs the exchange-butterfly kernels (taco_xk.cuh)
+inline bool xk_family() { return kernel_family() == 0; }
 
 // A zeroed device counter for one launch of a dynamically scheduled kernel (ring of
 // counters per device; each kernel leaves its counter at zero when it finishes).

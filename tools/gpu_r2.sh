@@ -20,7 +20,7 @@ fi
 if [ -n "${NCU:-}" ]; then
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file "$OUT/launches.csv" \
       python bench.py --steps 4 --warmup 3 --no-cpu-baseline --headline-only > "$OUT/ncu_bench.log" 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(compress|decompress)' -s 8 -c 2 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:'k_(compress|decompress)|k[12]x' -s 8 -c 2 \
       -o "$OUT/prof" -f python bench.py --steps 4 --warmup 3 --no-cpu-baseline --headline-only > "$OUT/ncu_full.log" 2>&1
   ncu -i "$OUT/prof.ncu-rep" --page raw --csv > "$OUT/raw.csv" 2>/dev/null
 fi
