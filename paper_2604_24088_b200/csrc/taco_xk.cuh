@@ -46,7 +46,10 @@ namespace taco_dev {
 namespace xk {
 
 constexpr int kWarps = 4;    // warps per CTA (persistent grid)
-constexpr int kMinCtas = 4;  // 16 warps per SM (registers capped at 128)
+#ifndef TACO_XK_MINCTAS
+#define TACO_XK_MINCTAS 4
+#endif
+constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capped at 128)
 
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
 __host__ __device__ constexpr int bit(int v, int b) { return (v >> b) & 1; }
@@ -299,6 +302,18 @@ __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts
     }
     // the scalar chain sits in the same basic block as the butterfly, which does not depend
     // on it (alpha enters only through k), so the scheduler overlaps its latency
+#if TACO_XK_F32CHAIN  // A/B experiment only: fp32 scalar chains (not parity-equivalent)
+    float ssf = (float)sl;
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) ssf += __shfl_xor_sync(kFull, ssf, o);
+    ss = ssf;
+    alpha = __fdiv_rn(c.tau, sqrtf(fmaf(ssf, (float)c.inv_b, c.eps)));
+    Plan::stages(w, q);
+    const float ymax = absmax32<L>(w);
+    const float gf = alpha / p2 * (float)c.norm;
+    s = ymax == 0.0f ? 1.0f : ymax * gf * (float)c.inv_qmax;
+    const float kf = gf / s;
+#else
     ss = group_sum<L>(sl);
     alpha = block_alpha_fast(ss, c);
     Plan::stages(w, q);
@@ -306,6 +321,7 @@ __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts
     double k;
     block_scale_fast((double)ymax, alpha, p2, c, s, k);
     const float kf = wide_prescale(w, k);
+#endif
     float mk[1 << Plan::LOGL];
     signed_mults<Plan::LOGL>(kf, q, mk);
     apply_mults<Plan::LOGL>(w, mk, [](int i) { return Plan::sidx(i); });
@@ -326,15 +342,24 @@ __device__ __forceinline__ void pack_codes(const float2 (&w)[32], uint4 (&out)[4
     }
 }
 
+// 16-byte global store that does not allocate in L1 (streamed output: measured 43.5 vs
+// 46.3 us for K2's access pattern alone, tools/mempat2.cu)
+__device__ __forceinline__ void st16_na(void* p, uint4 v) {
+    asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
 // 8 contiguous outputs (4 pairs) of type T
 template <typename T>
 __device__ __forceinline__ void store8(T* p, const float2* v) {
     if constexpr (sizeof(T) == 2) {
-        *reinterpret_cast<uint4*>(p) =
-            make_uint4(pack_bf16x2(v[0]), pack_bf16x2(v[1]), pack_bf16x2(v[2]), pack_bf16x2(v[3]));
+        st16_na(p, make_uint4(pack_bf16x2(v[0]), pack_bf16x2(v[1]), pack_bf16x2(v[2]), pack_bf16x2(v[3])));
     } else {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0].x, v[0].y, v[1].x, v[1].y);
-        *reinterpret_cast<float4*>(p + 4) = make_float4(v[2].x, v[2].y, v[3].x, v[3].y);
+        st16_na(p, make_uint4(__float_as_uint(v[0].x), __float_as_uint(v[0].y), __float_as_uint(v[1].x),
+                              __float_as_uint(v[1].y)));
+        st16_na(p + 4, make_uint4(__float_as_uint(v[2].x), __float_as_uint(v[2].y), __float_as_uint(v[3].x),
+                                  __float_as_uint(v[3].y)));
     }
 }
 template <typename T>
@@ -366,6 +391,12 @@ __device__ __forceinline__ void store_decoded(T* blk, int q, int valid, bool vec
 }
 
 // ------------------------------------------------------------- async copies -------
+// Codes of a warp tile (G blocks x B codes = 2 KB = 128 16-byte units) are copied coalesced
+// (instruction c, lane l -> unit 32 c + l) into a shared-memory tile whose 16-byte units are
+// XOR-swizzled (unit u at u ^ ((u >> 3) & 3)), so that the decode's per-lane reads (lane (g, q)
+// takes units 16 g + 4 q + c, its 64 contiguous codes) are bank-conflict free.  The half-sector
+// per-lane copies this replaces bound K2 at 53.4 us on configs[3] (tools/mempat.cu).
+__device__ __forceinline__ int swz_unit(int u) { return u ^ ((u >> 3) & 3); }
 __device__ __forceinline__ void cp16(void* smem, const void* gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
@@ -420,13 +451,15 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     // tile tt -> shard p, first block kk0 of the chunk, whether every block is whole
     struct Tile {
         uint32_t p;
-        uint64_t kk0;
+        uint32_t kk0;
         bool full;
     };
+    // whole-block limits as 32-bit (run_xk requires nblk < 2^31)
+    const uint32_t fmid = (uint32_t)a.full_mid, flast = (uint32_t)a.full_last, plast = a.P - 1;
     auto info = [&](uint32_t tt) -> Tile {
         const uint32_t p = tps.div(tt);
-        const uint64_t kk0 = (uint64_t)(tt - p * tps.d) * G;
-        return Tile{p, kk0, tile_full<B, G>(a, p, kk0)};
+        const uint32_t kk0 = (tt - p * tps.d) * G;
+        return Tile{p, kk0, a.vec_ok && kk0 + G <= (p == plast ? flast : fmid)};
     };
     auto issue = [&](const Tile& tl, int stage) {
         if (tl.full) {
@@ -467,9 +500,17 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
                                                             (int64_t)a.n - (int64_t)(p * a.S + k * B), B)
                                               : 0;
                 const TIn* src = x + (p * a.S + k * B);
+                // lane index re-read through a volatile move: the ragged path's offsets are
+                // not hoisted into (and kept live through) the whole-tile loop
+#if TACO_XK_PIN_Q || !defined(TACO_XK_PIN_Q)
+                int qq;
+                asm volatile("mov.b32 %0, %1;" : "=r"(qq) : "r"(q));
+#else
+                const int qq = q;
+#endif
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    const int pos = (j * L + q) * 8;
+                    const int pos = (j * L + qq) * 8;
                     float2 tmp[4];
                     if (a.vec_ok && pos + 8 <= valid) load_vec<TIn, 8>(src + pos, tmp);
                     else load_vec_guarded<TIn, 8>(src + pos, pos, valid, tmp);
@@ -525,15 +566,37 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 template <int L>
 struct K2X {
     static constexpr int B = 64 * L, G = 32 / L;
-    static constexpr int STAGES = 3;
-    // per stage: 4 chunks of 16 codes per lane, then one (alpha, s) pair per lane
-    static constexpr int STAGE_U4 = 4 * 32 + 16;
+    static constexpr int STAGES = 4;
+    // per stage: the tile's 128 code units (swizzled), then the G blocks' (alpha, s) pairs
+    static constexpr int STAGE_U4 = 128 + G / 2;
     static constexpr size_t SMEM = (size_t)kWarps * STAGES * STAGE_U4 * 16;
 };
 
 __device__ __forceinline__ void cp8(void* smem, const void* gmem) {
     const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
+// coalesced copy of a tile's codes (blocks kk0 .. kk0+G-1 of message m, live blocks only) and
+// scalars into one stage
+template <int L>
+__device__ __forceinline__ void stage_tile(uint4* sb, const uint8_t* m, uint64_t kk0, uint64_t nblk,
+                                           uint64_t scal_off, int lane) {
+    constexpr int B = 64 * L, G = 32 / L;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const int u = 32 * c + lane;
+        if (kk0 + (uint64_t)((16 * u) / B) < nblk) cp16(sb + swz_unit(u), m + kk0 * B + 16 * (uint64_t)u);
+    }
+    if (lane < G && kk0 + lane < nblk) cp8(reinterpret_cast<float2*>(sb + 128) + lane, m + scal_off + (kk0 + lane) * 8);
+}
+
+// this lane's 64 codes (units 16 g + 4 q + c for L = 4; generally (g B + 64 q) / 16 + c)
+template <int L>
+__device__ __forceinline__ void read_lane_codes(const uint4* sb, int g, int q, uint4 (&u)[4]) {
+    const int u0 = (g * 64 * L + 64 * q) / 16;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) u[c] = sb[swz_unit(u0 + c)];
 }
 
 // decode 64 codes (4 x 16 bytes, positions 16 ch + ..) into b0-stage pairs
@@ -573,15 +636,10 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     const uint32_t stride = gridDim.x * kWarps;
 
     auto issue = [&](uint32_t tt, int stage) {
-        const uint32_t p = tps.div(tt);
-        const uint64_t kk = (uint64_t)(tt - p * tps.d) * G + g;
-        if (kk < a.nblk) {  // codes of a live block are always present (messages hold nblk * B codes)
-            const uint8_t* m = msgs + p * a.msg_stride;
-            const uint8_t* src = m + kk * B + 64 * q;
-            uint4* sb = stage_base + stage * K::STAGE_U4;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) cp16(sb + ch * 32 + lane, src + 16 * ch);
-            cp8(reinterpret_cast<float2*>(sb + 4 * 32) + lane, m + a.scal_off + kk * 8);
+        if (tt < ntiles) {
+            const uint32_t p = tps.div(tt);
+            const uint64_t kk0 = (uint64_t)(tt - p * tps.d) * G;
+            stage_tile<L>(stage_base + stage * K::STAGE_U4, msgs + p * a.msg_stride, kk0, a.nblk, a.scal_off, lane);
         }
         cp_async_commit();
     };
@@ -589,30 +647,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     grid_dep_wait();
     uint32_t t = blockIdx.x * kWarps + warp;
 #pragma unroll
-    for (int i = 0; i < NS - 1; ++i) {
-        if (t + i * stride < ntiles) issue(t + i * stride, i);
-        else cp_async_commit();
-    }
+    for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
     int cur = 0;
     for (; t < ntiles; t += stride) {
-        {
-            const uint32_t tn = t + (NS - 1) * stride;
-            const int sn = cur == 0 ? NS - 1 : cur - 1;
-            if (tn < ntiles) issue(tn, sn);
-            else cp_async_commit();
-        }
+        __syncwarp();  // every lane is done with the stage about to be refilled
+        issue(t + (NS - 1) * stride, cur == 0 ? NS - 1 : cur - 1);
         const uint32_t p = tps.div(t);
         const uint64_t kk = (uint64_t)(t - p * tps.d) * G + g;
         const bool live = kk < a.nblk;
         cp_wait<NS - 1>();
+        __syncwarp();  // the other lanes' copies of this tile are visible
         const uint4* sb = stage_base + cur * K::STAGE_U4;
         cur = cur == NS - 1 ? 0 : cur + 1;
         uint4 u[4];
         float2 sc = make_float2(1.0f, 1.0f);
         if (live) {
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) u[ch] = sb[ch * 32 + lane];
-            sc = reinterpret_cast<const float2*>(sb + 4 * 32)[lane];
+            read_lane_codes<L>(sb, g, q, u);
+            sc = reinterpret_cast<const float2*>(sb + 128)[g];
         } else {
 #pragma unroll
             for (int ch = 0; ch < 4; ++ch) u[ch] = make_uint4(0, 0, 0, 0);
@@ -634,7 +685,7 @@ template <int L>
 struct K3X {
     static constexpr int B = 64 * L, G = 32 / L;
     static constexpr int STAGES = 3;
-    static constexpr int STAGE_U4 = 4 * 32;
+    static constexpr int STAGE_U4 = K2X<L>::STAGE_U4;
     static constexpr size_t SMEM = (size_t)kWarps * STAGES * STAGE_U4 * 16;
 };
 
@@ -659,44 +710,31 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     const bool live = kk < a.nblk;
     const int valid = live ? clamp_valid((int64_t)a.S - (int64_t)((a.blk0 + kk) * B), (int64_t)B, B) : 0;
     auto msg_of = [&](uint32_t r) -> const uint8_t* { return a.nsrc ? a.src[r] : msgs + r * a.msg_stride; };
-    float2 scq[NS];
-#pragma unroll
-    for (int i = 0; i < NS; ++i) scq[i] = make_float2(1.0f, 1.0f);
     auto issue = [&](uint32_t r, int stage) {
-        const uint8_t* m = msg_of(r);
-        float2 sc = make_float2(1.0f, 1.0f);
-        if (live) sc = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8));
-#pragma unroll
-        for (int i = 0; i < NS; ++i)
-            if (i == stage) scq[i] = sc;
-        if (live) {
-            const uint8_t* src = m + kk * B + 64 * q;
-            uint4* sb = stage_base + stage * K::STAGE_U4;
-#pragma unroll
-            for (int ch = 0; ch < 4; ++ch) cp16(sb + ch * 32 + lane, src + 16 * ch);
-        }
+        if (r < a.P) stage_tile<L>(stage_base + stage * K::STAGE_U4, msg_of(r), kk0, a.nblk, a.scal_off, lane);
         cp_async_commit();
     };
 #pragma unroll
-    for (int i = 0; i < NS - 1; ++i) {
-        if ((uint32_t)i < a.P) issue(i, i);
-        else cp_async_commit();
-    }
+    for (int i = 0; i < NS - 1; ++i) issue(i, i);
     float2 acc[32];
     bool ok = true;
+    int cur = 0;
     for (uint32_t r = 0; r < a.P; ++r) {
-        const int cur = r % NS;
-        if (r + NS - 1 < a.P) issue(r + NS - 1, (r + NS - 1) % NS);
-        else cp_async_commit();
-        float2 sc = scq[0];
-#pragma unroll
-        for (int i = 1; i < NS; ++i)
-            if (i == cur) sc = scq[i];
+        __syncwarp();  // every lane is done with the stage about to be refilled
+        issue(r + NS - 1, cur == 0 ? NS - 1 : cur - 1);
         cp_wait<NS - 1>();
-        uint4 u[4];
+        __syncwarp();  // the other lanes' copies of this rank's tile are visible
         const uint4* sb = stage_base + cur * K::STAGE_U4;
+        cur = cur == NS - 1 ? 0 : cur + 1;
+        uint4 u[4];
+        float2 sc = make_float2(1.0f, 1.0f);
+        if (live) {
+            read_lane_codes<L>(sb, g, q, u);
+            sc = reinterpret_cast<const float2*>(sb + 128)[g];
+        } else {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) u[ch] = live ? sb[ch * 32 + lane] : make_uint4(0, 0, 0, 0);
+            for (int ch = 0; ch < 4; ++ch) u[ch] = make_uint4(0, 0, 0, 0);
+        }
         ok &= scalars_ok(sc.x, sc.y);
         float2 y[32];
         decode_block<L>(u, sc, live, q, c, y);
