@@ -302,18 +302,6 @@ __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts
     }
     // the scalar chain sits in the same basic block as the butterfly, which does not depend
     // on it (alpha enters only through k), so the scheduler overlaps its latency
-#if TACO_XK_F32CHAIN  // A/B experiment only: fp32 scalar chains (not parity-equivalent)
-    float ssf = (float)sl;
-#pragma unroll
-    for (int o = 1; o < L; o <<= 1) ssf += __shfl_xor_sync(kFull, ssf, o);
-    ss = ssf;
-    alpha = __fdiv_rn(c.tau, sqrtf(fmaf(ssf, (float)c.inv_b, c.eps)));
-    Plan::stages(w, q);
-    const float ymax = absmax32<L>(w);
-    const float gf = alpha / p2 * (float)c.norm;
-    s = ymax == 0.0f ? 1.0f : ymax * gf * (float)c.inv_qmax;
-    const float kf = gf / s;
-#else
     ss = group_sum<L>(sl);
     alpha = block_alpha_fast(ss, c);
     Plan::stages(w, q);
@@ -321,7 +309,6 @@ __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts
     double k;
     block_scale_fast((double)ymax, alpha, p2, c, s, k);
     const float kf = wide_prescale(w, k);
-#endif
     float mk[1 << Plan::LOGL];
     signed_mults<Plan::LOGL>(kf, q, mk);
     apply_mults<Plan::LOGL>(w, mk, [](int i) { return Plan::sidx(i); });
@@ -414,7 +401,16 @@ struct K1X {
     static constexpr int NCH = 64 / EPC;              // chunks per lane per tile
     static constexpr int STAGES = 2;
     static constexpr int STAGE_U4 = NCH * 32;
-    static constexpr size_t SMEM = (size_t)kWarps * STAGES * STAGE_U4 * 16;
+#ifndef TACO_XK_CSTORE
+#define TACO_XK_CSTORE 1  // codes staged through shared memory: 54.0 -> 51.4 us (configs[3], bf16)
+#endif
+#if TACO_XK_CSTORE
+    static constexpr int CODE_U4 = 128;  // the tile's codes, staged for coalesced stores
+#else
+    static constexpr int CODE_U4 = 0;
+#endif
+    static constexpr int WARP_U4 = STAGES * STAGE_U4 + CODE_U4;
+    static constexpr size_t SMEM = (size_t)kWarps * WARP_U4 * 16;
     // element offset (in the block) of chunk ch of lane q: vector j = ch / (8 / EPC)
     __device__ static __forceinline__ int chunk_off(int ch, int q) {
         constexpr int CPV = 8 / EPC;
@@ -442,7 +438,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     constexpr int B = K::B, G = K::G, NCH = K::NCH, EPC = K::EPC;
     extern __shared__ uint4 smem_dyn[];
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
-    uint4* stage_base = smem_dyn + (size_t)warp * K::STAGES * K::STAGE_U4 + lane;
+    uint4* stage_base = smem_dyn + (size_t)warp * K::WARP_U4 + lane;
+    uint4* code_buf = smem_dyn + (size_t)warp * K::WARP_U4 + K::STAGES * K::STAGE_U4;
     const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kWarps;
     const int qoff = q * 8;  // lane's element offset inside a vector row (chunk_off(0, q))
@@ -502,12 +499,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
                 const TIn* src = x + (p * a.S + k * B);
                 // lane index re-read through a volatile move: the ragged path's offsets are
                 // not hoisted into (and kept live through) the whole-tile loop
-#if TACO_XK_PIN_Q || !defined(TACO_XK_PIN_Q)
                 int qq;
                 asm volatile("mov.b32 %0, %1;" : "=r"(qq) : "r"(q));
-#else
-                const int qq = q;
-#endif
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int pos = (j * L + qq) * 8;
@@ -538,6 +531,39 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         float alpha, s;
         double ss;
         encode<L, Plan>(w, q, c, alpha, s, ss, load_plain);
+#if TACO_XK_CSTORE
+        {
+            uint4 cv[4];
+            pack_codes<Plan>(w, cv);
+            const int u0 = (g * B + Plan::lane_off(q)) / 16;
+            __syncwarp();  // the previous tile's codes were read out
+#pragma unroll
+            for (int u = 0; u < 4; ++u) code_buf[swz_unit(u0 + u)] = cv[u];
+            __syncwarp();
+            uint4 ov[4];
+#pragma unroll
+            for (int c4 = 0; c4 < 4; ++c4) ov[c4] = code_buf[swz_unit(32 * c4 + lane)];
+            const uint64_t kk0 = cur.kk0;
+            auto put = [&](uint8_t* m) {
+#pragma unroll
+                for (int c4 = 0; c4 < 4; ++c4) {
+                    const int u = 32 * c4 + lane;
+                    if (full || kk0 + (uint64_t)((16 * u) / B) < a.nblk) st16_na(m + kk0 * B + 16 * (uint64_t)u, ov[c4]);
+                }
+                if (q == 0 && (full || kk < a.nblk))
+                    *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
+            };
+            if constexpr (PUSH) {
+                if (a.bcast)
+                    for (uint32_t d = 0; d < a.ndst; ++d) put(a.dst[d]);
+                else
+                    put(a.dst[p]);
+            } else {
+                put(msgs + p * a.msg_stride);
+            }
+            if (q == 0 && (full || kk < a.nblk) && !isfinite(ss)) raise_flag(a.flags, 1);
+        }
+#else
         if (full || kk < a.nblk) {
             uint4 cv[4];
             pack_codes<Plan>(w, cv);
@@ -558,6 +584,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
             }
             if (q == 0 && !isfinite(ss)) raise_flag(a.flags, 1);  // any NaN/Inf element poisons the block sum
         }
+#endif
         cur = nxt;
     }
 }
