@@ -33,7 +33,7 @@ template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
-        if (xk_family()) return run_xk<B / 64, T>(l, a, c);
+        if (xk_family() && a.nblk < (1ull << 31)) return run_xk<B / 64, T>(l, a, c);
     }
     if constexpr (FMT == 0 && B >= 64 && B <= 512) {
         // measured (profiles/README.md): tile kernels for B >= 256 and fp32 output at

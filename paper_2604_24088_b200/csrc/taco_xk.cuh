@@ -713,7 +713,8 @@ struct K3X {
     static constexpr int B = 64 * L, G = 32 / L;
     static constexpr int STAGES = 3;
     static constexpr int STAGE_U4 = K2X<L>::STAGE_U4;
-    static constexpr size_t SMEM = (size_t)kWarps * STAGES * STAGE_U4 * 16;
+    static constexpr int WARP_U4 = STAGES * STAGE_U4 + 128;  // + the re-encoded codes, staged
+    static constexpr size_t SMEM = (size_t)kWarps * WARP_U4 * 16;
 };
 
 // K3 holds the running sum and one decoded rank at once (2 x 64 values): 3 CTAs per SM
@@ -729,7 +730,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     constexpr int B = K::B, G = K::G, NS = K::STAGES;
     extern __shared__ uint4 smem_dyn[];
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
-    uint4* stage_base = smem_dyn + (size_t)warp * NS * K::STAGE_U4;
+    uint4* stage_base = smem_dyn + (size_t)warp * K::WARP_U4;
+    uint4* code_buf = stage_base + NS * K::STAGE_U4;
     const uint64_t kk0 = ((uint64_t)blockIdx.x * kWarps + warp) * G;
     grid_dep_wait();
     if (kk0 >= a.nblk) return;  // warp-uniform
@@ -819,18 +821,25 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     encode<L, Plan>(acc, q, c, alpha, s, ss, reload);
     uint4 cv[4];
     pack_codes<Plan>(acc, cv);
-    const int elo = Plan::lane_off(q);
-    const uint32_t nd = a.ndst ? a.ndst : 1;
-    if (live) {
-        for (uint32_t d = 0; d < nd; ++d) {  // peer mode: the same message into every rank's buffer
-            uint8_t* o = a.ndst ? a.dst[d] : out_msg;
-            uint4* dst = reinterpret_cast<uint4*>(o + kk * B + elo);
+    // codes staged through shared memory and stored coalesced (as K1)
+    const int u0 = (g * B + Plan::lane_off(q)) / 16;
 #pragma unroll
-            for (int u = 0; u < 4; ++u) dst[u] = cv[u];
-            if (q == 0) *reinterpret_cast<float2*>(o + a.scal_off + kk * 8) = make_float2(alpha, s);
+    for (int u = 0; u < 4; ++u) code_buf[swz_unit(u0 + u)] = cv[u];
+    __syncwarp();
+    uint4 ov[4];
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) ov[c4] = code_buf[swz_unit(32 * c4 + lane)];
+    const uint32_t nd = a.ndst ? a.ndst : 1;
+    for (uint32_t d = 0; d < nd; ++d) {  // peer mode: the same message into every rank's buffer
+        uint8_t* o = a.ndst ? a.dst[d] : out_msg;
+#pragma unroll
+        for (int c4 = 0; c4 < 4; ++c4) {
+            const int u = 32 * c4 + lane;
+            if (kk0 + (uint64_t)((16 * u) / B) < a.nblk) st16_na(o + kk0 * B + 16 * (uint64_t)u, ov[c4]);
         }
-        if (q == 0 && !ok) raise_flag(a.flags, 2);
+        if (live && q == 0) *reinterpret_cast<float2*>(o + a.scal_off + kk * 8) = make_float2(alpha, s);
     }
+    if (live && q == 0 && !ok) raise_flag(a.flags, 2);
 }
 
 }  // namespace xk
