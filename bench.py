@@ -461,6 +461,12 @@ def main():
     ap.add_argument("--headline-only", action="store_true", help="N=1: skip the other configs' tensors")
     ap.add_argument("--chunks", type=int, default=2, help="N>1: pipelined chunks per shard")
     ap.add_argument("--eager", action="store_true", help="N>1: no CUDA-graph capture of the step")
+    ap.add_argument("--nccl-nvls", type=int, default=None, choices=(0, 1),
+                    help="N>1: NCCL_NVLS_ENABLE for the communicator (the bf16 comparator without / with NVLS)")
+    ap.add_argument("--block-sweep", type=lambda t: [int(v) for v in t.split(",")], default=[32, 64, 128, 256, 512],
+                    help="N>1 configs[2]: Hadamard block sizes of the sequence-parallel sweep")
+    ap.add_argument("--size-sweep", type=lambda t: [float(v) for v in t.split(",")] if t else [], default=None,
+                    help="N>1: configs[4] message sizes in MB (default 1,16,256 at N>1; empty string disables)")
     ap.add_argument("--collective", action="store_true", help="run the collective leg even at world size 1")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=None,
                     help="BASELINE.json configs index of the per-rank tensor (N=1 default: 3, the largest; "
@@ -469,6 +475,8 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.size_sweep is None:
+        args.size_sweep = [1.0, 16.0, 256.0] if (world > 1 or args.collective) else []
     rank = int(os.environ.get("RANK", "0"))
     n_ranks = max(world, args.gpus) if args.impl == "reference" else world
     if args.shape:

@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import os
 import statistics
+import sys
 import time
 
 import torch
@@ -82,8 +83,8 @@ def _timed(fn, steps, stream):
 def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
     """Peer-memory two-shot (K1/K3 store into CUDA-IPC mapped peer regions, device
     barriers): time it like the NCCL leg and check it against the NCCL leg's result."""
-    from . import collective, peer
-    from ._abi import TacoError
+    from paper_2604_24088_b200 import collective, peer
+    from paper_2604_24088_b200._abi import TacoError
 
     world = dist.get_world_size()
     try:
@@ -138,11 +139,11 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
             "gpu_launches_per_step": 5, "barriers_per_step": 2}
 
 
-def _sp_leg(args, n, cfg, xs, stream, use_graphs):
+def _sp_leg(args, n, cfg, xs, stream, use_graphs, peer_leg=True):
     """CompressedReduceScatter of the [n] tensor and CompressedAllGather of its [n/P] slice,
     timed like the all-reduce, next to dist.reduce_scatter_tensor / all_gather_into_tensor
     bf16 on the same tensors."""
-    from . import collective
+    from paper_2604_24088_b200 import collective
 
     world = dist.get_world_size()
     dev = xs[0].device
@@ -175,9 +176,11 @@ def _sp_leg(args, n, cfg, xs, stream, use_graphs):
                      "wire_bytes_per_rank": (rs if name == "reduce_scatter" else ag).wire_bytes_per_rank()}
     rs.ar.codec.check()
     ag.codec.check()
+    if not peer_leg:
+        return rep
     # the same pair over peer memory (peer.py), checked bit for bit against the NCCL transport
-    from . import peer
-    from ._abi import TacoError
+    from paper_2604_24088_b200 import peer
+    from paper_2604_24088_b200._abi import TacoError
     try:
         prs = peer.PeerReduceScatter(n, cfg, dtype=torch.bfloat16, device=dev, timeout_ms=20_000)
         pag = peer.PeerAllGather(S, cfg, dtype=torch.bfloat16, device=dev, timeout_ms=20_000)
@@ -218,51 +221,62 @@ def _sp_leg(args, n, cfg, xs, stream, use_graphs):
     return rep
 
 
-def run_collective(args, rows, cols, clock_sampler, peaks):
-    from . import _abi, collective
-    from ._abi import make_config
+def _nccl_logging() -> str | None:
+    """NCCL INIT lines go to a per-process file (and stay out of rank 0's stdout, which is
+    the one JSON line); returns the file name, read back for the algorithm record."""
+    if "NCCL_DEBUG" in os.environ:
+        return os.environ.get("NCCL_DEBUG_FILE")
+    path = f"/tmp/taco_nccl_init.{os.getpid()}.log"
+    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,ENV", NCCL_DEBUG_FILE=path)
+    return path
 
-    if "RANK" not in os.environ:  # `bench.py --collective` without torchrun: a world of one
-        import socket
-        sk = socket.socket()
-        sk.bind(("127.0.0.1", 0))
-        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
-                          MASTER_PORT=str(sk.getsockname()[1]))
-        sk.close()
-    os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
-    world, rank = dist.get_world_size(), dist.get_rank()
-    n = rows * cols
-    cfg = make_config(args.block_size)
-    g = torch.Generator(device=dev).manual_seed(100 + rank)
-    R = 3  # rotate inputs / outputs so consecutive steps do not hit the same L2 lines
-    xs = []
-    for _ in range(R):
-        x = (torch.randn(n, generator=g, device=dev) * 1e-3)
-        x.index_fill_(0, torch.randint(0, n, (n // 100,), device=dev, generator=g), 1.0)
-        xs.append(x.to(torch.bfloat16))
-    outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(R)]
-    ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=dev)
-    stream = torch.cuda.current_stream()
-    graphs, launch_note = None, "eager"
+
+def _nccl_record(path: str | None) -> dict:
+    """What NCCL chose on this box: version, NVLS (NVLink SHARP multicast) availability and the
+    environment toggles that were set, from the INIT log (echoed to stderr for the driver)."""
+    rec = {"version": ".".join(str(v) for v in torch.cuda.nccl.version()),
+           "NCCL_DEBUG": os.environ.get("NCCL_DEBUG"),
+           "NCCL_NVLS_ENABLE": os.environ.get("NCCL_NVLS_ENABLE", "default"),
+           "NCCL_ALGO": os.environ.get("NCCL_ALGO", "default")}
+    if path and os.path.exists(path):
+        lines = open(path, errors="replace").read().splitlines()
+        for ln in lines:
+            print(ln, file=sys.stderr)
+        nv = [ln.split("NCCL INFO", 1)[-1].strip() for ln in lines if "NVLS" in ln or "nvls" in ln]
+        rec["nvls_lines"] = nv[:4]
+        rec["nvls_available"] = any("support is available" in ln or "NVLS multicast" in ln for ln in nv)
+    return rec
+
+
+def _inputs(n: int, rank: int, dev, R: int, scale: float = 1.0):
+    """The reference generator's near-zero mixture (taco::generate, seed 100 + rank as
+    acceptance.cpp:380), rounded to bf16, R rotations (distinct addresses, same values)."""
+    from paper_2604_24088_b200 import codec
+
+    x0 = codec.generate(codec.NEAR_ZERO_MIXTURE, n, 100 + rank).mul_(scale).to(torch.bfloat16).to(dev)
+    return [x0] + [torch.roll(x0, (k * n) // R // 256 * 256) for k in range(1, R)]
+
+
+def _ar_leg(args, n, cfg, xs, outs, stream, chunks):
+    """Compressed two-shot all-reduce (NCCL transport) timed over K steps, CUDA-graph captured
+    where every rank can, next to ncclAllReduce bf16 on the same tensors."""
+    from paper_2604_24088_b200 import collective
+
+    world = dist.get_world_size()
+    R = len(xs)
+    ar = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, chunks=chunks, device=xs[0].device)
+    graphs, note = None, "eager"
     if not args.eager:
-        # CUDA-graph capture of the step (kernels + NCCL); every rank takes the same path
         try:
-            graphs = [collective.Graphed(ar, xs[i], outs[i]) for i in range(R)]
-            ok = 1
-        except Exception as e:  # noqa: BLE001 -- reported in the JSON line, eager instead
-            graphs, ok, launch_note = None, 0, f"eager (graph capture failed: {type(e).__name__})"
-        t = torch.tensor([ok], device=dev)
+            graphs, ok = [collective.Graphed(ar, xs[i], outs[i]) for i in range(R)], 1
+        except Exception as e:  # noqa: BLE001 -- reported, eager instead
+            graphs, ok, note = None, 0, f"eager (graph capture failed: {type(e).__name__})"
+        t = torch.tensor([ok], device=xs[0].device)
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         if int(t.item()) == 1:
-            launch_note = "cuda_graph"
+            note = "cuda_graph"
         else:
             graphs = None
-            if launch_note == "eager":
-                launch_note = "eager (graph capture failed on another rank)"
 
     def step(i):
         if graphs is not None:
@@ -274,18 +288,8 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
         step(i)
     torch.cuda.synchronize()
     ar.codec.check()
-    with clock_sampler(local) as clk:
-        ms = _timed(step, args.steps, stream)
-        t0 = time.perf_counter()
-        while len(clk.rows) < 5 and time.perf_counter() - t0 < 5:
-            for i in range(20):
-                step(i)
-            torch.cuda.synchronize()
+    ms = _timed(step, args.steps, stream) / args.steps
     ar.codec.check()
-    step_ms = ms / args.steps
-    value = world * 2 * n / (step_ms * 1e-3) / 1e9
-
-    # uncompressed comparator: ncclAllReduce bf16 on the same tensors
     scratch = [x.clone() for x in xs]
 
     def nccl_step(i):
@@ -294,19 +298,97 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     for i in range(args.warmup):
         nccl_step(i)
     nccl_ms = _timed(nccl_step, args.steps, stream) / args.steps
+    wire = ar.wire_bytes_per_rank()
+    return ar, step, graphs, note, {
+        "ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
+        "nccl_bf16_ms_per_step": round(nccl_ms, 5),
+        "nccl_bf16_algbw_GBps": round(world * 2 * n / (nccl_ms * 1e-3) / 1e9, 1),
+        "speedup_vs_nccl_bf16": round(nccl_ms / ms, 3),
+        "wire_bytes_per_rank": wire, "wire_frac_of_nvlink_900": round(wire / (ms * 1e-3) / 900e9, 4),
+        "chunks": chunks, "launch": note}
+
+
+def run_collective(args, rows, cols, clock_sampler, peaks):
+    from paper_2604_24088_b200._abi import make_config
+
+    if "RANK" not in os.environ:  # `bench.py --collective` without torchrun: a world of one
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(RANK="0", WORLD_SIZE="1", LOCAL_RANK="0", MASTER_ADDR="127.0.0.1",
+                          MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
+    if args.nccl_nvls is not None:  # read by NCCL at communicator init
+        os.environ["NCCL_NVLS_ENABLE"] = str(args.nccl_nvls)
+    log = _nccl_logging()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    world, rank = dist.get_world_size(), dist.get_rank()
+    idx = args.config
+    n = rows * cols
+    cfg = make_config(args.block_size)
+    R = 3  # rotating inputs / outputs: consecutive steps do not hit the same L2 lines
+    xs = _inputs(n, rank, dev, R)
+    outs = [torch.empty(n, dtype=torch.bfloat16, device=dev) for _ in range(R)]
+    stream = torch.cuda.current_stream()
+    with clock_sampler(local) as clk:
+        ar, step, graphs, note, ar_rep = _ar_leg(args, n, cfg, xs, outs, stream, args.chunks)
+        t0 = time.perf_counter()
+        while len(clk.rows) < 5 and time.perf_counter() - t0 < 5:
+            for i in range(20):
+                step(i)
+            torch.cuda.synchronize()
+    step_ms = ar_rep["ms_per_step"]
+    value = world * 2 * n / (step_ms * 1e-3) / 1e9
 
     # the same all-reduce with the exchange done by the kernels' own stores into the peers'
     # memory (peer.py): no NCCL call on the data path; must be bit-identical to the above
     peer_rep = _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R)
 
-    # the sequence-parallel pair on the same tensors, vs NCCL bf16 reduce-scatter / all-gather
-    sp_rep = _sp_leg(args, n, cfg, xs, stream, graphs is not None)
+    extra = {}
+    if idx == 2 or args.collective:
+        # configs[2]: the sequence-parallel pair, with the Hadamard block-size sweep
+        extra["sequence_parallel"] = _sp_leg(args, n, cfg, xs, stream, graphs is not None)
+        sweep = {}
+        for b in args.block_sweep:
+            if b == args.block_size:
+                continue
+            cb = make_config(b)
+            sp = _sp_leg(args, n, cb, xs, stream, graphs is not None, peer_leg=False)
+            sweep[str(b)] = {k: v["ms_per_step"] for k, v in sp.items()}
+        extra["sequence_parallel_block_sweep"] = sweep
+    if idx == 3 or args.collective:
+        # configs[3]: the backward activation-gradient all-reduce on the same shape: gradients
+        # ~2^-6 of the activations (dual-scale quantisation: alpha absorbs the scale, the
+        # codes and s are those of the forward tensor, test_codec.cpp:217-234), overlapped
+        # by the chunked pipeline
+        gx = [x.float().mul_(2.0 ** -6).to(torch.bfloat16) for x in xs]
+        gouts = [torch.empty_like(o) for o in outs]
+        _, _, _, gnote, g_rep = _ar_leg(args, n, cfg, gx, gouts, stream, args.chunks)
+        extra["backward_gradient_allreduce"] = g_rep
+        extra["fwd_plus_bwd_ms"] = round(step_ms + g_rep["ms_per_step"], 5)
+        extra["fwd_plus_bwd_nccl_bf16_ms"] = round(ar_rep["nccl_bf16_ms_per_step"] + g_rep["nccl_bf16_ms_per_step"], 5)
+    if args.size_sweep:
+        # configs[4] summary: compressed vs uncompressed all-reduce over message sizes
+        sw = {}
+        for mb in args.size_sweep:
+            m_el = max(world * 256, int(mb * 2 ** 20) // 2)
+            sx = _inputs(m_el, rank, dev, 2)
+            so = [torch.empty_like(v) for v in sx]
+            sargs = type(args)(**{**vars(args), "steps": max(5, min(args.steps, 20)), "warmup": 3})
+            _, _, _, _, r = _ar_leg(sargs, m_el, cfg, sx, so, stream, args.chunks)
+            sw[f"{mb}MB"] = {"taco_ms": r["ms_per_step"], "nccl_bf16_ms": r["nccl_bf16_ms_per_step"],
+                             "speedup": r["speedup_vs_nccl_bf16"], "wire_frac_of_nvlink_900": r["wire_frac_of_nvlink_900"]}
+            del sx, so
+        extra["message_size_sweep"] = sw
 
     # e2e: pinned host tensor -> H2D -> compressed all-reduce -> D2H, every step
+    from paper_2604_24088_b200 import collective
     xh = xs[0].cpu().pin_memory()
     yh = torch.empty(n, dtype=torch.bfloat16).pin_memory()
     xd = torch.empty_like(xs[0])
-
     g_e2e = collective.Graphed(ar, xd, outs[0]) if graphs is not None else None
 
     def e2e_step(i):
@@ -323,14 +405,15 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     e2e_ms = _timed(e2e_step, e2e_steps, stream) / e2e_steps
 
     # parity spot check across ranks: everyone holds the identical result
+    ar(xs[0], outs[0])
     chk = outs[0].float().sum().reshape(1)
     mx, mn = chk.clone(), chk.clone()
     dist.all_reduce(mx, op=dist.ReduceOp.MAX)
     dist.all_reduce(mn, op=dist.ReduceOp.MIN)
-    wire = ar.wire_bytes_per_rank()
     pk = peaks()
     line = None
     if rank == 0:
+        wire = ar_rep["wire_bytes_per_rank"]
         line = {
             "metric": "taco_twoshot_allreduce_algbw_GBps",
             "value": round(value, 1),
@@ -343,27 +426,25 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
             "scaling": "weak",
             "vs_baseline": None,
             "dtype": "bf16",
-            "data": "synthetic near-zero mixture (N(0,1e-3) + 1% unit tail), bf16, generated on device",
-            "config": {"workload": f"configs[1] tensor per rank, TP={world} FP8 two-shot all-reduce",
-                       "shape": [rows, cols], "elements_per_rank": n, "block_size": args.block_size,
-                       "format": "E4M3", "chunks": args.chunks, "parallelism": f"tp{world}",
-                       "launch": launch_note,
-                       "l2": f"{R} rotating input/output buffers of {2 * n / 1e6:.0f} MB"},
-            "nccl_bf16_allreduce": {"ms_per_step": round(nccl_ms, 5),
-                                    "algbw_GBps": round(world * 2 * n / (nccl_ms * 1e-3) / 1e9, 1),
-                                    "speedup_of_taco": round(nccl_ms / step_ms, 3)},
+            "data": "synthetic: taco::generate near-zero mixture (the reference generator), seed 100 + rank, bf16",
+            "config": {**workload_config(args, world), "chunks": args.chunks, "launch": note,
+                       "l2": f"{R} rotating input/output buffers of {2 * n / 1e6:.0f} MB per rank"},
+            "nccl_bf16_allreduce": {"ms_per_step": ar_rep["nccl_bf16_ms_per_step"],
+                                    "algbw_GBps": ar_rep["nccl_bf16_algbw_GBps"],
+                                    "speedup_of_taco": ar_rep["speedup_vs_nccl_bf16"]},
+            "nccl": _nccl_record(log),
             "wire": {"bytes_per_rank_per_direction": wire,
                      "GBps_per_rank": round(wire / (step_ms * 1e-3) / 1e9, 1),
-                     "frac_of_nvlink_900": round(wire / (step_ms * 1e-3) / 900e9, 4)},
+                     "frac_of_nvlink_900": ar_rep["wire_frac_of_nvlink_900"]},
             "roofline": {"bound": "nvlink", "achieved": round(wire / (step_ms * 1e-3) / 1e9, 1), "peak": 900.0,
-                         "unit": "GB/s", "frac": round(wire / (step_ms * 1e-3) / 900e9, 4), "traffic": None,
-                         "peak_source": "nominal NVLink 5 per direction (measured peer copy ~770)",
+                         "unit": "GB/s", "frac": ar_rep["wire_frac_of_nvlink_900"], "traffic": None,
+                         "peak_source": "nominal NVLink 5 per direction",
                          "hbm_peak_GBps": pk["hbm_gbs"]},
             "e2e": {"value": round(world * 2 * n / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GB/s",
                     "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n,
                     "api": "collective.TwoShotAllReduce (pinned host in / out)"},
             "peer_memory_twoshot": peer_rep,
-            "sequence_parallel": sp_rep,
+            **extra,
             "ranks_agree": bool(abs(float(mx.item()) - float(mn.item())) == 0.0),
             "gpu_launches": 3 * len(ar.ch.ranges) * args.steps,
             "clocks": clk.summary(),
