@@ -74,7 +74,9 @@ def peaks() -> dict:
 
 def ncu_traffic(kind: str):
     """dram read + write bytes per launch of the K1 ('compress') / K2 ('decompress') kernel
-    from the newest committed ncu capture (profiles/*_ncu_traffic.json), or None."""
+    from the newest committed ncu capture (profiles/*_ncu_traffic.json), or None.  The
+    capture's L2 write bytes ride along: dram writes miss the stores still dirty in L2 when a
+    single replayed launch ends, L2 writes count every store."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu_traffic.json")))
     if not files:
@@ -83,8 +85,10 @@ def ncu_traffic(kind: str):
         with open(files[-1]) as f:
             d = json.load(f)
         for k in d["kernels"]:
-            if kind in k.get("role", k["kernel"]):
+            if k.get("role", k["kernel"]) == kind:
                 return {"bytes": int(k["dram_read_bytes"] + k["dram_write_bytes"]), "kernel": k["kernel"],
+                        "dram_read_bytes": int(k["dram_read_bytes"]), "dram_write_bytes": int(k["dram_write_bytes"]),
+                        "l2_write_bytes": int(k["l2_write_bytes"]) if k.get("l2_write_bytes") else None,
                         "source": os.path.relpath(files[-1], ROOT), "note": d.get("note", "")}
     except Exception:
         return None

@@ -279,6 +279,15 @@ int taco_roundtrip_host(taco_ctx* ctx, const taco_config* cfg, const void* x_hos
 int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* inputs_host,
                             uint32_t nranks, uint64_t n, float* result_host, float* stage1_host);
 
+/* taco::allreduce (collective.hpp:28) for every Algorithm (0 TwoShot, 1 Ring, 2 Tree;
+ * collective.cpp:75-111, :116-134, :153-254) on host rank tensors inputs [P][n] f32,
+ * computed on the device: result[n] (identical on every rank), exact[n] = the fp32 sum in
+ * ascending rank order (collective.cpp:36-41), rel_l2 (optional) = relative L2 of result
+ * against exact (the error_vs_frequency column, collective.cpp:270-294). */
+int taco_allreduce_schedule_host(taco_ctx* ctx, const taco_config* cfg, int algorithm,
+                                 const float* inputs_host, uint32_t nranks, uint64_t n,
+                                 float* result_host, float* exact_host, double* rel_l2);
+
 /* taco::scaled_spectrum (codec.hpp:70) of a host tensor: ceil(n/B)*B fp32 values */
 int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float* x_host, uint64_t n,
                               float* out_host);

@@ -107,6 +107,7 @@ _SIGNATURES = {
     "taco_decompress_host": (C.c_int, [_P, C.POINTER(Config), _P, _U64, _P, _I]),
     "taco_roundtrip_host": (C.c_int, [_P, C.POINTER(Config), _P, _I, _U64, _P, _I]),
     "taco_allreduce_sim_host": (C.c_int, [_P, C.POINTER(Config), _P, _U32, _U64, _P, _P]),
+    "taco_allreduce_schedule_host": (C.c_int, [_P, C.POINTER(Config), C.c_int, _P, _U32, _U64, _P, _P, _P]),
     "taco_scaled_spectrum_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _P, _P]),
     "taco_archive_header": (C.c_int, [C.POINTER(Config), _U64, _P]),
     "taco_archive_export_dev": (C.c_int, [C.POINTER(Config), _P, _U64, _P, _P]),

@@ -729,6 +729,8 @@ struct taco_ctx {
     void* h_stage_in[kSlots] = {};
     void* h_stage_out[kSlots] = {};
     size_t cap_stage_in = 0, cap_stage_out = 0;
+    void* d_scratch = nullptr;  // grow-only workspace of the one-shot host calls (allreduce_sim, spectrum)
+    size_t cap_scratch = 0;
     std::mutex mu;
 };
 
@@ -823,8 +825,33 @@ void taco_ctx_destroy(taco_ctx* c) {
         if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
     }
     cudaFree(c->d_flags);
+    cudaFree(c->d_scratch);
     delete c;
 }
+
+namespace {
+// Carves `count` 256-byte-aligned regions of the given sizes out of the context's grow-only
+// scratch buffer: repeated host calls of the same (or a smaller) size never allocate, and
+// the buffer is reallocated only after the context's streams drained.
+int ctx_scratch(taco_ctx* ctx, const size_t* sizes, void** out, int count) {
+    size_t total = 0;
+    for (int i = 0; i < count; ++i) total += (sizes[i] + 255) & ~size_t(255);
+    if (total > ctx->cap_scratch) {
+        for (int i = 0; i < taco_ctx::kSlots; ++i) TACO_CUDA(cudaStreamSynchronize(ctx->st[i]));
+        cudaFree(ctx->d_scratch);
+        ctx->d_scratch = nullptr;
+        ctx->cap_scratch = 0;
+        TACO_CUDA(cudaMalloc(&ctx->d_scratch, total));
+        ctx->cap_scratch = total;
+    }
+    auto* p = static_cast<uint8_t*>(ctx->d_scratch);
+    for (int i = 0; i < count; ++i) {
+        out[i] = sizes[i] ? p : nullptr;
+        p += (sizes[i] + 255) & ~size_t(255);
+    }
+    return TACO_OK;
+}
+}  // namespace
 
 // Shared driver of the three host calls.  mode 0 = compress, 1 = decompress, 2 = round trip.
 static int host_pipeline(taco_ctx* ctx, const taco_config* cfg, int mode, const void* src, int in_dtype,
@@ -990,12 +1017,13 @@ int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float
     DeviceGuard dg(ctx->device);
     TACO_CUDA(dg.err);
     const uint64_t out_n = div_up(n, cfg->block_size) * cfg->block_size;
-    void *d_in = nullptr, *d_out = nullptr;
+    void* bufs[2] = {};
+    const size_t sizes[2] = {n * 4, out_n * 4};
+    if (int rc = ctx_scratch(ctx, sizes, bufs, 2)) return rc;
+    void *d_in = bufs[0], *d_out = bufs[1];
     cudaStream_t st = ctx->st[0];
     int rc = TACO_OK;
-    cudaError_t e = cudaMalloc(&d_in, n * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&d_out, out_n * 4);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
+    cudaError_t e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, x_host, n * 4, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "scaled spectrum staging");
     if (rc == TACO_OK) rc = taco_scaled_spectrum_dev(cfg, d_in, TACO_DT_F32, n, static_cast<float*>(d_out), ctx->d_flags, st);
@@ -1009,8 +1037,6 @@ int taco_scaled_spectrum_host(taco_ctx* ctx, const taco_config* cfg, const float
         e = cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
         rc = e != cudaSuccess ? cuda_fail(e, "flags readback") : taco_flags_status(flags);
     }
-    cudaFree(d_in);
-    cudaFree(d_out);
     return rc;
 }
 
@@ -1026,14 +1052,13 @@ int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* 
     const uint64_t S = div_up(n, nranks);
     const size_t in_bytes = (size_t)nranks * n * 4, st_bytes = stage1_host ? (size_t)nranks * S * 4 : 0;
     const size_t ws = taco_allreduce_sim_workspace(cfg, nranks, n);
-    void *d_in = nullptr, *d_out = nullptr, *d_st = nullptr, *d_ws = nullptr;
+    void* bufs[4] = {};
+    const size_t sizes[4] = {in_bytes, n * 4, st_bytes, ws};
+    if (int rc = ctx_scratch(ctx, sizes, bufs, 4)) return rc;
+    void *d_in = bufs[0], *d_out = bufs[1], *d_st = bufs[2], *d_ws = bufs[3];
     cudaStream_t st = ctx->st[0];
     int rc = TACO_OK;
-    cudaError_t e = cudaMalloc(&d_in, in_bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&d_out, n * 4);
-    if (e == cudaSuccess && st_bytes) e = cudaMalloc(&d_st, st_bytes);
-    if (e == cudaSuccess) e = cudaMalloc(&d_ws, ws);
-    if (e == cudaSuccess) e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
+    cudaError_t e = cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_in, inputs_host, in_bytes, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) rc = cuda_fail(e, "allreduce staging");
     if (rc == TACO_OK)
@@ -1050,11 +1075,134 @@ int taco_allreduce_sim_host(taco_ctx* ctx, const taco_config* cfg, const float* 
         e = cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost);
         rc = e != cudaSuccess ? cuda_fail(e, "flags readback") : taco_flags_status(flags);
     }
-    cudaFree(d_in);
-    cudaFree(d_out);
-    cudaFree(d_st);
-    cudaFree(d_ws);
     return rc;
+}
+
+// taco::allreduce (collective.cpp:75-254) for all three schedules on host rank tensors,
+// computed on the device.  Every "rank" tensor lives in one [P][padded] fp32 array; a ring
+// or tree transfer is a compress + decompress of the moved range in place (the codec grid
+// starts at the range start, as the reference's through_codec of a slice), and every fp32
+// sum is a device add in ascending-origin order.  The host only walks the schedule's range
+// bookkeeping.  exact_host receives the ascending-rank fp32 sum; rel_l2 (optional) the
+// relative L2 of result vs exact (taco_error_report_dev's definition, analysis.cpp:97-124).
+int taco_allreduce_schedule_host(taco_ctx* ctx, const taco_config* cfg, int algorithm, const float* inputs_host,
+                                 uint32_t nranks, uint64_t n, float* result_host, float* exact_host,
+                                 double* rel_l2) {
+    if (!ctx) return fail(TACO_ERR_USAGE, "null taco context");
+    if (nranks < 2) return fail(TACO_ERR_USAGE, "allreduce needs at least 2 ranks");
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    if (algorithm < 0 || algorithm > 2) return fail(TACO_ERR_USAGE, "unknown allreduce algorithm");
+    if (!inputs_host || !result_host || !exact_host) return fail(TACO_ERR_USAGE, "allreduce needs host buffers");
+    if (int rc = check_config(cfg)) return rc;
+    std::lock_guard<std::mutex> lock(ctx->mu);
+    DeviceGuard dg(ctx->device);
+    TACO_CUDA(dg.err);
+    const uint64_t P = nranks;
+    uint64_t q = 1;
+    while (2 * q <= P) q *= 2;
+    const uint64_t padded = div_up(n, q) * q, slice = padded / q;
+    const taco_layout lay = layout_of(payload_of(cfg), div_up(padded, cfg->block_size));
+    void* bufs[6] = {};
+    const size_t sizes[6] = {P * padded * 4, P * padded * 4, padded * 4, padded * 4, q * lay.msg_stride,
+                             algorithm == 0 ? taco_allreduce_sim_workspace(cfg, nranks, n) : 0};
+    if (int rc = ctx_scratch(ctx, sizes, bufs, 6)) return rc;
+    float* in = static_cast<float*>(bufs[0]);    // [P][padded] rank inputs, zero-padded
+    float* data = static_cast<float*>(bufs[1]);  // [P][padded] per-origin working copies
+    float* exact = static_cast<float*>(bufs[2]);
+    float* result = static_cast<float*>(bufs[3]);
+    uint8_t* msg = static_cast<uint8_t*>(bufs[4]);
+    cudaStream_t st = ctx->st[0];
+    TACO_CUDA(cudaMemsetAsync(ctx->d_flags, 0, sizeof(int), st));
+    TACO_CUDA(cudaMemsetAsync(in, 0, sizes[0], st));
+    TACO_CUDA(cudaMemcpy2DAsync(in, padded * 4, inputs_host, n * 4, n * 4, P, cudaMemcpyHostToDevice, st));
+    auto add = [&](float* a, const float* b, uint64_t len) -> int {
+        if (cudaError_t e = taco_impl::launch_add_f32(a, b, len, st)) return cuda_fail(e, "fp32 sum launch");
+        return TACO_OK;
+    };
+    // what the receiving rank reconstructs from one transfer of x[0, len): in place
+    auto through_codec = [&](float* x, uint64_t len) -> int {
+        const uint64_t m = div_up(len, cfg->block_size);
+        if (int rc = taco_compress_dev(cfg, x, TACO_DT_F32, len, 1, 0, m, msg, lay.msg_stride, ctx->d_flags, st))
+            return rc;
+        return taco_decompress_dev(cfg, msg, lay.msg_stride, 1, len, 0, m, x, TACO_DT_F32, ctx->d_flags, st);
+    };
+    auto copy = [&](float* dst, const float* src, uint64_t len) -> int {
+        TACO_CUDA(cudaMemcpyAsync(dst, src, len * 4, cudaMemcpyDeviceToDevice, st));
+        return TACO_OK;
+    };
+    // exact: fp32 sum over ranks in ascending rank order (collective.cpp:36-41)
+    int rc = copy(exact, in, padded);
+    for (uint64_t r = 1; r < P && rc == TACO_OK; ++r) rc = add(exact, in + r * padded, padded);
+    if (rc == TACO_OK && algorithm == 0) {
+        // two-shot: the fused K1 -> K3 -> K2 simulation over a dense [P][n] copy
+        TACO_CUDA(cudaMemcpy2DAsync(data, n * 4, in, padded * 4, n * 4, P, cudaMemcpyDeviceToDevice, st));
+        rc = taco_allreduce_sim_dev(cfg, data, TACO_DT_F32, nranks, n, result, TACO_DT_F32, nullptr, bufs[5],
+                                    ctx->d_flags, st);
+    } else if (rc == TACO_OK && algorithm == 1) {
+        // ring: the partial climbs the ranks; every hop crosses the codec, then the next
+        // rank adds its own input; the total is compressed once and forwarded unchanged
+        rc = copy(result, in, n);
+        for (uint64_t r = 1; r < P && rc == TACO_OK; ++r) {
+            rc = through_codec(result, n);
+            if (rc == TACO_OK) rc = add(result, in + r * padded, n);
+        }
+        if (rc == TACO_OK) rc = through_codec(result, n);
+    } else if (rc == TACO_OK) {
+        // tree: origin o's values stay in data[o]; at[r] is where rank r's current range
+        // starts and held[r] the origins it carries.  A halving round moves every carried
+        // origin's far half to the partner through the codec.
+        rc = copy(data, in, P * padded);
+        std::vector<std::vector<uint32_t>> held(q);
+        std::vector<uint64_t> at(q, 0);
+        for (uint64_t r = 0; r < q; ++r) held[r].push_back((uint32_t)r);
+        for (uint64_t j = q; j < P && rc == TACO_OK; ++j) {  // fold the excess ranks into rank j - q
+            rc = through_codec(data + j * padded, padded);
+            held[j - q].push_back((uint32_t)j);
+        }
+        for (uint64_t h = q / 2, len = padded; h >= 1 && rc == TACO_OK; h /= 2, len /= 2) {
+            const uint64_t half = len / 2;
+            std::vector<std::vector<uint32_t>> next = held;
+            for (uint64_t r = 0; r < q && rc == TACO_OK; ++r) {
+                const uint64_t far = at[r] + ((r & h) ? 0 : half);
+                for (uint32_t o : held[r]) {
+                    if ((rc = through_codec(data + o * padded + far, half))) break;
+                    next[r ^ h].push_back(o);
+                }
+            }
+            for (uint64_t r = 0; r < q; ++r) at[r] += (r & h) ? half : 0;
+            held.swap(next);
+        }
+        // every rank holds all P origins over slice r: one ascending-origin sum for all
+        // slices at once, then every slice is compressed at its owner and decoded once
+        if (rc == TACO_OK) rc = copy(result, data, padded);
+        for (uint64_t o = 1; o < P && rc == TACO_OK; ++o) rc = add(result, data + o * padded, padded);
+        const uint64_t ms = div_up(slice, cfg->block_size);
+        const taco_layout sl = layout_of(payload_of(cfg), ms);
+        if (rc == TACO_OK)
+            rc = taco_compress_dev(cfg, result, TACO_DT_F32, padded, (uint32_t)q, 0, ms, msg, sl.msg_stride,
+                                   ctx->d_flags, st);
+        if (rc == TACO_OK)
+            rc = taco_decompress_dev(cfg, msg, sl.msg_stride, (uint32_t)q, padded, 0, ms, result, TACO_DT_F32,
+                                     ctx->d_flags, st);
+    }
+    if (rc != TACO_OK) {
+        cudaStreamSynchronize(st);
+        return rc;
+    }
+    TACO_CUDA(cudaMemcpyAsync(exact_host, exact, n * 4, cudaMemcpyDeviceToHost, st));
+    TACO_CUDA(cudaMemcpyAsync(result_host, result, n * 4, cudaMemcpyDeviceToHost, st));
+    TACO_CUDA(cudaStreamSynchronize(st));
+    int flags = 0;
+    TACO_CUDA(cudaMemcpy(&flags, ctx->d_flags, sizeof(int), cudaMemcpyDeviceToHost));
+    if (int frc = taco_flags_status(flags)) return frc;
+    if (rel_l2) {
+        taco_error_report rep;
+        uint64_t count = 0;
+        if (int erc = taco_error_report_dev(exact, TACO_DT_F32, result, TACO_DT_F32, n, 1, &rep, &count, st))
+            return erc;
+        *rel_l2 = rep.relative_l2;
+    }
+    return TACO_OK;
 }
 
 }  // extern "C"

@@ -302,106 +302,37 @@ uint64_t message_bytes(const CodecConfig& cfg, uint64_t n, size_t chunk_elements
 
 namespace {
 
-// what a receiving rank reconstructs from one compressed transfer (device codec)
-TensorBuffer round_trip(const TensorBuffer& x, const CodecConfig& cfg) { return decompress(compress(x, cfg)); }
-
-// Ring (collective.cpp:112-134): the running partial walks up the ranks in ascending
-// order, crossing every hop through the codec; the receiving rank adds its own input in
-// fp32.  The last rank compresses the total once and that archive is forwarded P-1 hops
-// unchanged, so every rank decodes the same bytes.
-TensorBuffer ring_schedule(const RankSet& rs, uint64_t& steps, uint64_t& bytes) {
-    const size_t P = rs.inputs.size(), n = rs.inputs[0].size();
-    const uint64_t hop = message_bytes(rs.codec, n, rs.chunk_elements);
-    TensorBuffer run = rs.inputs[0];
-    for (size_t r = 1; r < P; ++r) {
-        run = round_trip(run, rs.codec);
-        for (size_t i = 0; i < n; ++i) run[i] += rs.inputs[r][i];
+// Schedule shape (collective.cpp:75-254) in closed form: compressed transfer steps and wire
+// bytes.  Two-shot: two batched steps of P(P-1) shard messages.  Ring: P-1 codec hops of the
+// whole tensor plus P-1 forwards of the final archive.  Tree over q = 2^floor(log2 P) ranks:
+// an optional fold step (P-q whole padded tensors), log2 q halving rounds in which each of the
+// P origins is carried as 2^k pieces of padded/2^(k+1) elements, log2 q doubling rounds in
+// which every rank forwards the 2^k slice archives it holds, and an optional unfold step.
+void schedule_shape(const RankSet& rs, uint64_t& steps, uint64_t& bytes) {
+    const uint64_t p = rs.inputs.size(), n = rs.inputs[0].size();
+    auto mb = [&](uint64_t len) { return message_bytes(rs.codec, len, rs.chunk_elements); };
+    steps = bytes = 0;
+    if (rs.algorithm == Algorithm::TwoShot) {
+        steps = 2;
+        bytes = 2 * p * (p - 1) * mb((n + p - 1) / p);
+        return;
     }
-    steps += 2 * (P - 1);
-    bytes += 2 * (P - 1) * hop;
-    return decompress(compress(run, rs.codec));
+    if (rs.algorithm == Algorithm::Ring) {
+        steps = 2 * (p - 1);
+        bytes = 2 * (p - 1) * mb(n);
+        return;
+    }
+    uint64_t q = 1, levels = 0;
+    while (2 * q <= p) q *= 2, ++levels;
+    const uint64_t padded = (n + q - 1) / q * q, slice = padded / q, extra = p - q;
+    steps = 2 * levels + (extra ? 2 : 0);
+    bytes = extra * mb(padded) + extra * q * mb(slice);
+    for (uint64_t k = 0, pieces = p, len = padded / 2; k < levels; ++k, pieces *= 2, len /= 2)
+        bytes += pieces * mb(len);
+    for (uint64_t k = 0, held = 1; k < levels; ++k, held *= 2) bytes += q * held * mb(slice);
 }
 
-// Tree (collective.cpp:153-254): recursive halving that keeps every origin's
-// contribution separate (each transfer round-trips every carried piece through the
-// codec), an ascending-origin fp32 sum per final slice compressed once, then recursive
-// doubling of those slice archives.  Ranks beyond the largest power of two fold their
-// whole input into rank j first and receive the assembled result at the end.
-TensorBuffer tree_schedule(const RankSet& rs, uint64_t& steps, uint64_t& bytes) {
-    const size_t P = rs.inputs.size(), n = rs.inputs[0].size();
-    size_t q = 1;
-    while (2 * q <= P) q *= 2;
-    const size_t extra = P - q;
-    const size_t padded = (n + q - 1) / q * q, slice = padded / q;
-    auto padded_input = [&](size_t r) {
-        TensorBuffer v = rs.inputs[r];
-        v.resize(padded, 0.0f);
-        return v;
-    };
-    // pieces[r]: (origin, values over rank r's current range)
-    std::vector<std::vector<std::pair<size_t, TensorBuffer>>> pieces(q);
-    for (size_t r = 0; r < q; ++r) pieces[r].emplace_back(r, padded_input(r));
-    if (extra) {
-        for (size_t j = 0; j < extra; ++j) {
-            pieces[j].emplace_back(q + j, round_trip(padded_input(q + j), rs.codec));
-            bytes += message_bytes(rs.codec, padded, rs.chunk_elements);
-        }
-        steps += 1;
-    }
-    for (size_t h = q / 2, len = padded; h >= 1; h /= 2) {
-        const size_t half = len / 2;
-        std::vector<std::vector<std::pair<size_t, TensorBuffer>>> recv(q);
-        for (size_t r = 0; r < q; ++r) {
-            const bool low = (r & h) == 0;  // r keeps the low half, its partner the high one
-            for (const auto& pc : pieces[r]) {
-                const auto from = pc.second.begin() + static_cast<ptrdiff_t>(low ? half : 0);
-                recv[r ^ h].emplace_back(pc.first, round_trip(TensorBuffer(from, from + half), rs.codec));
-                bytes += message_bytes(rs.codec, half, rs.chunk_elements);
-            }
-        }
-        steps += 1;
-        for (size_t r = 0; r < q; ++r) {
-            const size_t at = (r & h) == 0 ? 0 : half;
-            for (auto& pc : pieces[r])
-                pc.second = TensorBuffer(pc.second.begin() + at, pc.second.begin() + at + half);
-            for (auto& pc : recv[r]) pieces[r].push_back(std::move(pc));
-        }
-        len = half;
-        if (h == 1) break;
-    }
-    // rank r now owns slice r with all P origins: sum in ascending origin order
-    std::vector<CompressedTensor> owned(q);
-    for (size_t r = 0; r < q; ++r) {
-        auto& v = pieces[r];
-        std::sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
-        TensorBuffer acc = v[0].second;
-        for (size_t c = 1; c < v.size(); ++c)
-            for (size_t i = 0; i < slice; ++i) acc[i] += v[c].second[i];
-        owned[r] = compress(acc, rs.codec);
-    }
-    // recursive doubling of slice archives (never re-encoded): rank r holds 2^k of them
-    // after k rounds; account the transfers, then assemble rank 0's copy in slice order
-    for (size_t h = 1, have = 1; h < q; h *= 2, have *= 2) {
-        bytes += (uint64_t)q * have * message_bytes(rs.codec, slice, rs.chunk_elements);
-        steps += 1;
-    }
-    if (extra) {
-        bytes += (uint64_t)extra * q * message_bytes(rs.codec, slice, rs.chunk_elements);
-        steps += 1;
-    }
-    TensorBuffer result;
-    result.reserve(padded);
-    for (size_t r = 0; r < q; ++r) {
-        TensorBuffer part = decompress(owned[r]);
-        result.insert(result.end(), part.begin(), part.end());
-    }
-    result.resize(n);
-    return result;
-}
-
-}  // namespace
-
-AllReduceOutcome allreduce(const RankSet& rs) {
+AllReduceOutcome run_schedule(const RankSet& rs, double* rel_l2) {
     if (rs.inputs.size() < 2) fail(ErrorCode::Usage, "allreduce needs at least 2 ranks");
     const size_t n = rs.inputs[0].size();
     if (n == 0) fail(ErrorCode::Input, "input tensor is empty");
@@ -409,50 +340,37 @@ AllReduceOutcome allreduce(const RankSet& rs) {
         if (in.size() != n) fail(ErrorCode::Input, "all rank inputs must have the same length");
     validate_config(rs.codec);
     const size_t p = rs.inputs.size();
+    std::vector<float> flat(p * n);
+    for (size_t r = 0; r < p; ++r) std::copy(rs.inputs[r].begin(), rs.inputs[r].end(), flat.begin() + r * n);
     AllReduceOutcome out;
-    out.compress_invocations = 0;
-    out.bytes_on_wire = 0;
-    if (rs.algorithm == Algorithm::TwoShot) {
-        // the fused device schedule: K1 -> (exchange) -> K3 -> (exchange) -> K2
-        std::vector<float> flat(p * n);
-        for (size_t r = 0; r < p; ++r) std::copy(rs.inputs[r].begin(), rs.inputs[r].end(), flat.begin() + r * n);
-        out.result.resize(n);
-        const taco_config c = to_c(rs.codec);
-        check(taco_allreduce_sim_host(context(), &c, flat.data(), static_cast<uint32_t>(p), n, out.result.data(),
-                                      nullptr));
-        const uint64_t shard = (n + p - 1) / p;
-        out.compress_invocations = 2;
-        out.bytes_on_wire = 2ull * p * (p - 1) * message_bytes(rs.codec, shard, rs.chunk_elements);
-    } else if (rs.algorithm == Algorithm::Ring) {
-        out.result = ring_schedule(rs, out.compress_invocations, out.bytes_on_wire);
-    } else {
-        out.result = tree_schedule(rs, out.compress_invocations, out.bytes_on_wire);
-    }
-    out.exact = rs.inputs[0];  // fp32, ascending rank (collective.cpp:36-41)
-    for (size_t r = 1; r < p; ++r)
-        for (size_t i = 0; i < n; ++i) out.exact[i] += rs.inputs[r][i];
+    out.result.resize(n);
+    out.exact.resize(n);
+    const taco_config c = to_c(rs.codec);
+    check(taco_allreduce_schedule_host(context(), &c, static_cast<int>(rs.algorithm), flat.data(),
+                                       static_cast<uint32_t>(p), n, out.result.data(), out.exact.data(), rel_l2));
+    schedule_shape(rs, out.compress_invocations, out.bytes_on_wire);
     return out;
 }
 
-// collective.cpp:270-294: relative L2 of every schedule against the fp32 sum
+}  // namespace
+
+AllReduceOutcome allreduce(const RankSet& rs) { return run_schedule(rs, nullptr); }
+
+// collective.cpp:270-294: the three schedules on the same inputs; the relative L2 of each
+// comes from the device error report of its result against the exact sum.
 std::vector<AlgorithmRow> error_vs_frequency(const RankSet& rs) {
     std::vector<AlgorithmRow> rows;
     for (Algorithm a : {Algorithm::TwoShot, Algorithm::Ring, Algorithm::Tree}) {
         RankSet run = rs;
         run.algorithm = a;
-        const AllReduceOutcome o = allreduce(run);
-        double num = 0.0, den = 0.0;
-        for (size_t i = 0; i < o.result.size(); ++i) {
-            const double d = static_cast<double>(o.result[i]) - o.exact[i];
-            num += d * d;
-            den += static_cast<double>(o.exact[i]) * o.exact[i];
-        }
-        const double rel = den > 0.0 ? std::sqrt(num / den) : (num > 0.0 ? std::numeric_limits<double>::infinity() : 0.0);
-        rows.push_back({a, rel, o.compress_invocations, o.bytes_on_wire});
+        AlgorithmRow row{a, 0.0, 0, 0};
+        const AllReduceOutcome o = run_schedule(run, &row.relative_l2);
+        row.compress_invocations = o.compress_invocations;
+        row.bytes_on_wire = o.bytes_on_wire;
+        rows.push_back(row);
     }
-    if (rows[0].compress_invocations > rows[1].compress_invocations ||
-        rows[0].compress_invocations > rows[2].compress_invocations)
-        throw std::logic_error("twoshot must use the fewest compressed steps");
+    const uint64_t fewest = std::min(rows[1].compress_invocations, rows[2].compress_invocations);
+    if (rows[0].compress_invocations > fewest) throw std::logic_error("twoshot must use the fewest compressed steps");
     return rows;
 }
 

@@ -20,13 +20,25 @@ for r in rows[2:]:
             return None
     name = d["Kernel Name"]
     short = name.replace("void ", "").replace("taco_dev::", "").split("(")[0]
-    res.append({"kernel": short,
+    role = ("compress" if short.startswith(("k1x", "k_compress")) else
+            "decompress" if short.startswith(("k2x", "k_decompress")) else
+            "reduce_encode" if short.startswith(("k3x", "k_reduce")) else short)
+    l2w, l2r = f("lts__t_sectors_srcunit_tex_op_write.sum"), f("lts__t_sectors_srcunit_tex_op_read.sum")
+    res.append({"kernel": short, "role": role,
                 "dram_read_bytes": f("dram__bytes_read.sum"),
                 "dram_write_bytes": f("dram__bytes_write.sum"),
                 "duration_us": f("gpu__time_duration.sum"),
                 "registers": f("launch__registers_per_thread"),
                 "issue_active": f("smsp__issue_active.avg.per_cycle_active"),
-                "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active")})
-json.dump({"source": f"ncu --set full --clock-control none, {tag} (tools/gpu_round.sh), one launch each",
+                "warps_active_pct": f("sm__warps_active.avg.pct_of_peak_sustained_active"),
+                # every byte the SMs store reaches L2; DRAM write-back of the last ~L2-size of
+                # them happens after the launch ends, so L2 write bytes are the write traffic
+                "l2_write_bytes": 32 * l2w if l2w is not None else None,
+                "l2_read_bytes": 32 * l2r if l2r is not None else None,
+                "dram_pct_of_peak": f("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                "warp_instructions": f("smsp__inst_executed.sum")})
+json.dump({"source": f"ncu --set full --clock-control none, {tag}, one launch each",
+           "note": "dram_write_bytes misses the stores still dirty in L2 when the launch ends; "
+                   "l2_write_bytes counts every store",
            "kernels": res}, open(out, "w"), indent=1)
 print(json.dumps(res, indent=1))
