@@ -256,6 +256,107 @@ def measure_tensor(idx, rows, cols, dtype_name, args, dev, stream, clk=None):
     return out
 
 
+class CollectiveCodecBench:
+    """Per-rank codec work of one compressed two-shot all-reduce at P ranks (the collective
+    budget): K1 of the P shards of the rank tensor, K3 of the P received
+    copies of the own shard, K2 of the P gathered shards -- each timed alone over R rotating
+    buffer sets (every launch reads what the previous pass wrote >= one set ago: cold)."""
+
+    R = 3
+
+    def __init__(self, rows, cols, P, block_size, dev, seed=SEED):
+        import torch
+
+        from paper_2604_24088_b200 import _abi, codec
+        self.torch, self._abi = torch, _abi
+        self.n, self.P = rows * cols, P
+        self.cfg = codec.make_config(block_size)
+        self.S = -(-self.n // P)
+        self.m = -(-self.S // block_size)
+        self.lay = _abi.msg_layout(self.cfg, self.m)
+        x0 = codec.generate(MIXTURE, self.n, seed).to(dev).to(torch.bfloat16)
+        self.xs = [torch.roll(x0, k * block_size * 977) for k in range(self.R)]
+        st = self.lay.msg_stride
+        self.send = [torch.empty(P * st, dtype=torch.uint8, device=dev) for _ in range(self.R)]
+        self.red = [torch.empty(st, dtype=torch.uint8, device=dev) for _ in range(self.R)]
+        self.ys = [torch.empty(self.n, dtype=torch.bfloat16, device=dev) for _ in range(self.R)]
+        self.flags = codec.Flags(dev)
+        self.lib = _abi.lib()
+
+    def _st(self):
+        import ctypes as C
+        return C.c_void_p(self.torch.cuda.current_stream().cuda_stream)
+
+    def k1(self, i):
+        import ctypes as C
+        self._abi.check(self.lib.taco_compress_dev(
+            C.byref(self.cfg), C.c_void_p(self.xs[i].data_ptr()), self._abi.DT_BF16, self.n, self.P, 0, self.m,
+            C.c_void_p(self.send[i].data_ptr()), self.lay.msg_stride, self.flags.ptr(), self._st()))
+
+    def k3(self, i):
+        import ctypes as C
+        self._abi.check(self.lib.taco_reduce_encode_dev(
+            C.byref(self.cfg), C.c_void_p(self.send[i].data_ptr()), self.lay.msg_stride, self.P, self.S, 0, self.m,
+            C.c_void_p(self.red[i].data_ptr()), None, 0, self.flags.ptr(), self._st()))
+
+    def k2(self, i):
+        import ctypes as C
+        self._abi.check(self.lib.taco_decompress_dev(
+            C.byref(self.cfg), C.c_void_p(self.send[i].data_ptr()), self.lay.msg_stride, self.P, self.n, 0, self.m,
+            C.c_void_p(self.ys[i].data_ptr()), self._abi.DT_BF16, self.flags.ptr(), self._st()))
+
+    def measure(self, steps, stream) -> dict:
+        torch = self.torch
+        out = {}
+        with torch.cuda.stream(stream):
+            for i in range(self.R):
+                self.k1(i)
+                self.k3(i)
+                self.k2(i)
+            stream.synchronize()
+            self.flags.check()
+            for name in ("k1", "k3", "k2"):
+                fn = getattr(self, name)
+                g = _graph(lambda: [fn((s + 1) % self.R) for s in range(steps)], stream)
+                g.replay()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                stream.synchronize()
+                a.record(stream)
+                g.replay()
+                b.record(stream)
+                stream.synchronize()
+                out[name] = a.elapsed_time(b) / steps
+        self.flags.check()
+        return out
+
+
+def collective_budget(args, dev, stream, pk) -> dict:
+    """configs[1] TP=2, configs[2] TP=4, configs[3] TP=8: measured per-rank codec time of the
+    FP8 two-shot against the NVLink wire time of the FP8 two-shot and of a bf16 ring
+    all-reduce (both at the nominal 900 GB/s per direction: wire lower bounds)."""
+    nvlink = 900.0
+    res = {}
+    for idx, P in ((1, 2), (2, 4), (3, 8)):
+        r, c = CONFIGS[idx][:2]
+        cb = CollectiveCodecBench(r, c, P, args.block_size, dev)
+        t = cb.measure(max(10, min(args.steps, 50)), stream)
+        n, m, st = cb.n, cb.m, cb.lay
+        wire_fp8 = 2 * (P - 1) * st.msg_bytes  # bytes sent per rank per direction, both phases
+        wire_bf16 = 2 * (P - 1) * n * 2 / P  # ring all-reduce
+        k3_bytes = (P + 1) * st.msg_bytes
+        codec_us = (t["k1"] + t["k3"] + t["k2"]) * 1e3
+        res[f"configs{idx}_tp{P}"] = {
+            "shape": [r, c], "P": P,
+            "k1_us": round(t["k1"] * 1e3, 2), "k3_us": round(t["k3"] * 1e3, 2), "k2_us": round(t["k2"] * 1e3, 2),
+            "codec_us": round(codec_us, 2),
+            "k3_frac_of_hbm": round(k3_bytes / (t["k3"] * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
+            "fp8_wire_us_at_900GBps": round(wire_fp8 / (nvlink * 1e9) * 1e6, 2),
+            "bf16_ring_wire_us_at_900GBps": round(wire_bf16 / (nvlink * 1e9) * 1e6, 2),
+        }
+        del cb
+    return res
+
+
 def run_taco_single(args) -> dict:
     import torch
 
@@ -296,6 +397,9 @@ def run_taco_single(args) -> dict:
                 "k1_ms": round(e["k1_ms"], 5), "k1_frac": round(e["k1_gbs"] / pk["hbm_gbs"], 4),
                 "k2_ms": round(e["k2_ms"], 5), "k2_frac": round(e["k2_gbs"] / pk["hbm_gbs"], 4), **unit}
             del e
+
+    if not args.headline_only:
+        extras["collective_codec_budget"] = collective_budget(args, dev, stream, pk)
 
     # ---- e2e through the C-ABI host call (pinned host buffers, H2D + D2H inside the timed region)
     hc = codec.HostContext(0)

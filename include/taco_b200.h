@@ -166,21 +166,37 @@ int taco_scaled_spectrum_dev(const taco_config* cfg, const void* x, int dtype, u
 /* --------------------------------------------- collectives over a caller's NCCL communicator ---
  * The two-shot across real ranks (collective.cpp:75-111; SURVEY §8b taco_allreduce_twoshot),
  * one rank per GPU: K1 -> grouped ncclSend/ncclRecv (all-to-all of the FP8 messages) -> K3
- * -> ncclAllGather -> K2, all on `stream`.  `comm` is an ncclComm_t of P ranks (P = the shard
- * count); NCCL is resolved at run time from the process (the library does not link it).
- * work: taco_collective_nccl_workspace(cfg, P, n_total) bytes of device memory, n_total =
- * the full tensor (all-gather: P * n_local). */
+ * -> ncclAllGather -> K2.  `comm` is an ncclComm_t of P ranks (P = the shard count); NCCL is
+ * resolved at run time from the process (the library does not link it).
+ * Overlap: every shard is cut into `chunks` block-aligned chunks
+ * (numerics unchanged, test_collective.cpp:225-238; 0 = the default, 2; at most 16).  The codec
+ * kernels run on `stream`; the NCCL calls run on the library's communication stream of the
+ * device, ordered against `stream` by events both ways, so chunk c's transfer overlaps chunk
+ * c +- 1's kernels.  The call is CUDA-graph capturable (the communication stream is forked into
+ * and joined back from the capture).  The unsuffixed entry points use the default chunking.
+ * work: taco_collective_nccl_workspace[_chunked](cfg, P, n_total[, chunks]) bytes of device
+ * memory, n_total = the full tensor (all-gather: P * n_local), for the same chunk count. */
 uint64_t taco_collective_nccl_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n_total);
+uint64_t taco_collective_nccl_workspace_chunked(const taco_config* cfg, uint32_t nranks, uint64_t n_total,
+                                                uint32_t chunks);
 /* all-reduce: x[n] (dtype) -> out[n] (out_dtype), identical on every rank */
 int taco_allreduce_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out, int out_dtype,
                         void* work, void* comm, int* d_flags, void* stream);
+int taco_allreduce_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
+                                int out_dtype, void* work, void* comm, int* d_flags, void* stream, uint32_t chunks);
 /* sequence-parallel reduce-scatter: x[n] -> this rank's shard out[ceil(n/P)], the ascending-
  * rank fp32 sum of the decoded shard copies (collective.cpp:95-100), in out_dtype */
 int taco_reduce_scatter_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
                              int out_dtype, void* work, void* comm, int* d_flags, void* stream);
+int taco_reduce_scatter_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
+                                     int out_dtype, void* work, void* comm, int* d_flags, void* stream,
+                                     uint32_t chunks);
 /* sequence-parallel all-gather: x[n_local] -> out[P * n_local] (every rank's slice decoded) */
 int taco_all_gather_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n_local, void* out,
                          int out_dtype, void* work, void* comm, int* d_flags, void* stream);
+int taco_all_gather_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n_local, void* out,
+                                 int out_dtype, void* work, void* comm, int* d_flags, void* stream,
+                                 uint32_t chunks);
 
 /* ------------------------------------ peer-memory two-shot (SURVEY §8e, B200 extras) -----
  * The two-shot of collective.cpp:75-111 with the exchange folded into the kernels, no

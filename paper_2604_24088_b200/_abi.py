@@ -119,6 +119,10 @@ _SIGNATURES = {
     "taco_allreduce_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_reduce_scatter_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_all_gather_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
+    "taco_collective_nccl_workspace_chunked": (_U64, [C.POINTER(Config), _U32, _U64, _U32]),
+    "taco_allreduce_nccl_chunked": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P, _U32]),
+    "taco_reduce_scatter_nccl_chunked": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P, _U32]),
+    "taco_all_gather_nccl_chunked": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P, _U32]),
     "taco_peer_alloc": (C.c_int, [_I, _U64, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
     "taco_peer_open": (C.c_int, [_I, C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),
     "taco_peer_close": (C.c_int, [_P]),

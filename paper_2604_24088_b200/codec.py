@@ -348,3 +348,18 @@ class HostContext:
         _abi.check(_abi.lib().taco_allreduce_sim_host(self.h, C.byref(cfg), _ptr(inputs.contiguous()), p, n,
                                                       _ptr(res), _ptr(st)))
         return (res, st) if want_stage1 else res
+
+    def allreduce(self, inputs: torch.Tensor, cfg: Config, algorithm: int = 0):
+        """taco::allreduce(RankSet) for Algorithm 0 TwoShot / 1 Ring / 2 Tree on host rank tensors
+        [P][n] f32, computed on the device: (result, exact, relative_l2)."""
+        self._host(inputs, "rank inputs")
+        if inputs.dtype != torch.float32 or inputs.dim() != 2:
+            raise TacoError(_abi.ERR_USAGE, "rank inputs must be a [P][n] float32 tensor (taco::RankSet)")
+        p, n = inputs.shape
+        res = torch.empty(n, dtype=torch.float32)
+        exact = torch.empty(n, dtype=torch.float32)
+        rel = C.c_double(0.0)
+        _abi.check(_abi.lib().taco_allreduce_schedule_host(self.h, C.byref(cfg), int(algorithm),
+                                                           _ptr(inputs.contiguous()), p, n, _ptr(res), _ptr(exact),
+                                                           C.byref(rel)))
+        return res, exact, rel.value

@@ -11,6 +11,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <cuda_runtime.h>
+
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -70,6 +73,9 @@ int nfail(int code, const std::string& msg) { return taco_impl::set_error(code, 
 
 uint64_t div_up(uint64_t a, uint64_t b) { return (a + b - 1) / b; }
 
+constexpr uint32_t kMaxChunks = 16;
+constexpr uint32_t kDefaultChunks = 2;  // collective.py / bench.py default: two chunks per shard
+
 struct Geo {
     int P = 0, rank = 0;
     taco_layout lay{};
@@ -107,71 +113,239 @@ int all_to_all(const uint8_t* send, uint8_t* recv, uint64_t stride, uint64_t byt
     return nccl_check(n.group_end());
 }
 
+// Block-aligned chunks of every shard (blocks never span chunks, so numerics are unchanged,
+// test_collective.cpp:225-238) -- the same split as collective.py's _Chunking.
+struct Chunks {
+    int count = 0;
+    uint64_t b0[kMaxChunks] = {}, b1[kMaxChunks] = {};
+    taco_layout lay[kMaxChunks] = {};
+    uint64_t bytes_per_rank_slot = 0;  // sum of the chunk strides
+};
+
+int make_chunks(const taco_config* cfg, uint64_t m, uint32_t chunks, Chunks& ch) {
+    if (chunks == 0) chunks = kDefaultChunks;
+    if (chunks > kMaxChunks) return nfail(TACO_ERR_USAGE, "at most 16 pipelined chunks");
+    const uint64_t c = std::max<uint64_t>(1, std::min<uint64_t>(chunks, m));
+    const uint64_t per = div_up(m, c);
+    ch = Chunks{};
+    for (uint64_t b = 0; b < m; b += per) {
+        const int k = ch.count++;
+        ch.b0[k] = b;
+        ch.b1[k] = std::min(m, b + per);
+        if (int rc = taco_msg_layout(cfg, ch.b1[k] - ch.b0[k], &ch.lay[k])) return rc;
+        ch.bytes_per_rank_slot += ch.lay[k].msg_stride;
+    }
+    return TACO_OK;
+}
+
+// The communication side stream of a device and a pool of ordering events.  The codec
+// kernels stay on the caller's stream; every NCCL call goes to this stream, fenced by
+// events both ways, so chunk c's transfer overlaps chunk c +- 1's kernels.  Under CUDA-graph
+// capture of the caller's stream the event waits fork this stream into the capture and the
+// final wait joins it back.
+struct CommLane {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev[4 * kMaxChunks] = {};
+    int ready = 0;  // 1 ok, -1 failed
+};
+
+CommLane* comm_lane(int device) {
+    static std::mutex mu;
+    static CommLane* lanes[64] = {};
+    if (device < 0 || device >= 64) return nullptr;
+    std::lock_guard<std::mutex> lock(mu);
+    CommLane*& l = lanes[device];
+    if (!l) {
+        l = new CommLane();
+        bool ok = cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking) == cudaSuccess;
+        for (auto& e : l->ev) ok = ok && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess;
+        l->ready = ok ? 1 : -1;
+    }
+    return l->ready == 1 ? l : nullptr;
+}
+
+int cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return TACO_OK;
+    return nfail(TACO_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// `from` -> `to` ordering through event k
+int order(cudaStream_t from, cudaStream_t to, cudaEvent_t ev) {
+    if (int rc = cuda_check(cudaEventRecord(ev, from), "event record")) return rc;
+    return cuda_check(cudaStreamWaitEvent(to, ev, 0), "stream wait");
+}
+
+struct Lane {
+    CommLane* l = nullptr;
+    std::unique_lock<std::mutex> lock;
+    int open() {
+        int dev = 0;
+        if (int rc = cuda_check(cudaGetDevice(&dev), "current device")) return rc;
+        l = comm_lane(dev);
+        if (!l) return nfail(TACO_ERR_CUDA, "communication stream creation failed");
+        lock = std::unique_lock<std::mutex>(l->mu);
+        return TACO_OK;
+    }
+};
+
 }  // namespace
 
 extern "C" {
 
+uint64_t taco_collective_nccl_workspace_chunked(const taco_config* cfg, uint32_t nranks, uint64_t n,
+                                                uint32_t chunks) {
+    if (!cfg || nranks == 0 || n == 0 || cfg->block_size == 0 || chunks > kMaxChunks) return 0;
+    Chunks ch;
+    if (make_chunks(cfg, div_up(div_up(n, nranks), cfg->block_size), chunks, ch)) return 0;
+    return (3ull * nranks + 1) * ch.bytes_per_rank_slot;  // send, recv, gath [P][msg] + red [msg] per chunk
+}
+
 uint64_t taco_collective_nccl_workspace(const taco_config* cfg, uint32_t nranks, uint64_t n) {
-    if (!cfg || nranks == 0 || n == 0 || cfg->block_size == 0) return 0;
-    taco_layout lay{};
-    if (taco_msg_layout(cfg, div_up(div_up(n, nranks), cfg->block_size), &lay)) return 0;
-    return (3ull * nranks + 1) * lay.msg_stride;  // send, recv, gath [P][msg] + red [msg]
+    return taco_collective_nccl_workspace_chunked(cfg, nranks, n, kDefaultChunks);
+}
+
+int taco_allreduce_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
+                                int out_dtype, void* work, void* comm, int* d_flags, void* stream, uint32_t chunks) {
+    if (n == 0) return nfail(TACO_ERR_INPUT, "input tensor is empty");
+    Geo g;  // P is the communicator's size: query it first, then size the shards
+    if (int rc = comm_geo(cfg, comm, g)) return rc;
+    const uint64_t P = (uint64_t)g.P, S = div_up(n, P), m = div_up(S, cfg->block_size);
+    Chunks ch;
+    if (int rc = make_chunks(cfg, m, chunks, ch)) return rc;
+    if (!work) return nfail(TACO_ERR_USAGE, "workspace required (taco_collective_nccl_workspace bytes)");
+    Lane lane;
+    if (int rc = lane.open()) return rc;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream), ns = lane.l->stream;
+    cudaEvent_t* ev = lane.l->ev;
+    // per chunk: send [P][st], recv [P][st], gath [P][st], red [st]
+    uint8_t *send[kMaxChunks], *recv[kMaxChunks], *gath[kMaxChunks], *red[kMaxChunks];
+    uint8_t* at = static_cast<uint8_t*>(work);
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        send[c] = at, recv[c] = at + P * st, gath[c] = at + 2 * P * st, red[c] = at + 3 * P * st;
+        at += (3 * P + 1) * st;
+    }
+    auto nc = static_cast<ncclComm_t>(comm);
+    // phase 1: K1 of every chunk, its all-to-all in flight on the comm lane
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        if (int rc = taco_compress_dev(cfg, x, dtype, n, g.P, ch.b0[c], ch.b1[c], send[c], st, d_flags, stream))
+            return rc;
+        if (int rc = order(cs, ns, ev[c])) return rc;
+        if (int rc = all_to_all(send[c], recv[c], st, st, g, comm, ns)) return rc;
+    }
+    // owner reduce + re-encode as each chunk lands, the all-gather in flight
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        if (int rc = order(ns, cs, ev[kMaxChunks + c])) return rc;
+        if (int rc = taco_reduce_encode_dev(cfg, recv[c], st, g.P, S, ch.b0[c], ch.b1[c], red[c], nullptr, 0,
+                                            d_flags, stream))
+            return rc;
+        if (int rc = order(cs, ns, ev[2 * kMaxChunks + c])) return rc;
+        if (int rc = nccl_check(nccl().all_gather(red[c], gath[c], st, ncclUint8, nc, ns))) return rc;
+    }
+    for (int c = 0; c < ch.count; ++c) {
+        if (int rc = order(ns, cs, ev[3 * kMaxChunks + c])) return rc;
+        if (int rc = taco_decompress_dev(cfg, gath[c], ch.lay[c].msg_stride, g.P, n, ch.b0[c], ch.b1[c], out,
+                                         out_dtype, d_flags, stream))
+            return rc;
+    }
+    return TACO_OK;
 }
 
 int taco_allreduce_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out, int out_dtype,
                         void* work, void* comm, int* d_flags, void* stream) {
+    return taco_allreduce_nccl_chunked(cfg, x, dtype, n, out, out_dtype, work, comm, d_flags, stream,
+                                       kDefaultChunks);
+}
+
+int taco_reduce_scatter_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
+                                     int out_dtype, void* work, void* comm, int* d_flags, void* stream,
+                                     uint32_t chunks) {
     if (n == 0) return nfail(TACO_ERR_INPUT, "input tensor is empty");
-    Geo g;  // P is the communicator's size: query it first, then size the shards
+    Geo g;
     if (int rc = comm_geo(cfg, comm, g)) return rc;
-    const uint64_t S = div_up(n, (uint64_t)g.P), m = div_up(S, cfg->block_size);
-    if (int rc = taco_msg_layout(cfg, m, &g.lay)) return rc;
-    const uint64_t st = g.lay.msg_stride, P = (uint64_t)g.P;
+    const uint64_t P = (uint64_t)g.P, S = div_up(n, P), m = div_up(S, cfg->block_size);
+    Chunks ch;
+    if (int rc = make_chunks(cfg, m, chunks, ch)) return rc;
     if (!work) return nfail(TACO_ERR_USAGE, "workspace required (taco_collective_nccl_workspace bytes)");
-    uint8_t* send = static_cast<uint8_t*>(work);
-    uint8_t* recv = send + P * st;
-    uint8_t* gath = recv + P * st;
-    uint8_t* red = gath + P * st;
-    if (int rc = taco_compress_dev(cfg, x, dtype, n, g.P, 0, m, send, st, d_flags, stream)) return rc;
-    if (int rc = all_to_all(send, recv, st, st, g, comm, stream)) return rc;
-    if (int rc = taco_reduce_encode_dev(cfg, recv, st, g.P, S, 0, m, red, nullptr, 0, d_flags, stream)) return rc;
-    if (int rc = nccl_check(nccl().all_gather(red, gath, st, ncclUint8, static_cast<ncclComm_t>(comm),
-                                              static_cast<cudaStream_t>(stream))))
-        return rc;
-    return taco_decompress_dev(cfg, gath, st, g.P, n, 0, m, out, out_dtype, d_flags, stream);
+    Lane lane;
+    if (int rc = lane.open()) return rc;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream), ns = lane.l->stream;
+    cudaEvent_t* ev = lane.l->ev;
+    uint8_t *send[kMaxChunks], *recv[kMaxChunks];
+    uint8_t* at = static_cast<uint8_t*>(work);
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        send[c] = at, recv[c] = at + P * st;
+        at += 2 * P * st;
+    }
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        if (int rc = taco_compress_dev(cfg, x, dtype, n, g.P, ch.b0[c], ch.b1[c], send[c], st, d_flags, stream))
+            return rc;
+        if (int rc = order(cs, ns, ev[c])) return rc;
+        if (int rc = all_to_all(send[c], recv[c], st, st, g, comm, ns)) return rc;
+    }
+    for (int c = 0; c < ch.count; ++c) {
+        if (int rc = order(ns, cs, ev[kMaxChunks + c])) return rc;
+        if (int rc = taco_reduce_encode_dev(cfg, recv[c], ch.lay[c].msg_stride, g.P, S, ch.b0[c], ch.b1[c], nullptr,
+                                            out, out_dtype, d_flags, stream))
+            return rc;
+    }
+    return TACO_OK;
 }
 
 int taco_reduce_scatter_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n, void* out,
                              int out_dtype, void* work, void* comm, int* d_flags, void* stream) {
-    if (n == 0) return nfail(TACO_ERR_INPUT, "input tensor is empty");
+    return taco_reduce_scatter_nccl_chunked(cfg, x, dtype, n, out, out_dtype, work, comm, d_flags, stream,
+                                            kDefaultChunks);
+}
+
+int taco_all_gather_nccl_chunked(const taco_config* cfg, const void* x, int dtype, uint64_t n_local, void* out,
+                                 int out_dtype, void* work, void* comm, int* d_flags, void* stream,
+                                 uint32_t chunks) {
+    if (n_local == 0) return nfail(TACO_ERR_INPUT, "input tensor is empty");
     Geo g;
     if (int rc = comm_geo(cfg, comm, g)) return rc;
-    const uint64_t S = div_up(n, (uint64_t)g.P), m = div_up(S, cfg->block_size);
-    if (int rc = taco_msg_layout(cfg, m, &g.lay)) return rc;
-    const uint64_t st = g.lay.msg_stride, P = (uint64_t)g.P;
+    const uint64_t P = (uint64_t)g.P, m = div_up(n_local, cfg->block_size);
+    Chunks ch;
+    if (int rc = make_chunks(cfg, m, chunks, ch)) return rc;
     if (!work) return nfail(TACO_ERR_USAGE, "workspace required (taco_collective_nccl_workspace bytes)");
-    uint8_t* send = static_cast<uint8_t*>(work);
-    uint8_t* recv = send + P * st;
-    if (int rc = taco_compress_dev(cfg, x, dtype, n, g.P, 0, m, send, st, d_flags, stream)) return rc;
-    if (int rc = all_to_all(send, recv, st, st, g, comm, stream)) return rc;
-    return taco_reduce_encode_dev(cfg, recv, st, g.P, S, 0, m, nullptr, out, out_dtype, d_flags, stream);
+    Lane lane;
+    if (int rc = lane.open()) return rc;
+    cudaStream_t cs = static_cast<cudaStream_t>(stream), ns = lane.l->stream;
+    cudaEvent_t* ev = lane.l->ev;
+    uint8_t *mine[kMaxChunks], *gath[kMaxChunks];
+    uint8_t* at = static_cast<uint8_t*>(work);
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        mine[c] = at, gath[c] = at + st;
+        at += (P + 1) * st;
+    }
+    auto nc = static_cast<ncclComm_t>(comm);
+    for (int c = 0; c < ch.count; ++c) {
+        const uint64_t st = ch.lay[c].msg_stride;
+        if (int rc = taco_compress_dev(cfg, x, dtype, n_local, 1, ch.b0[c], ch.b1[c], mine[c], st, d_flags, stream))
+            return rc;
+        if (int rc = order(cs, ns, ev[c])) return rc;
+        if (int rc = nccl_check(nccl().all_gather(mine[c], gath[c], st, ncclUint8, nc, ns))) return rc;
+    }
+    for (int c = 0; c < ch.count; ++c) {
+        if (int rc = order(ns, cs, ev[kMaxChunks + c])) return rc;
+        // the gathered tensor is P shards of n_local: shard geometry S = n_local exactly
+        if (int rc = taco_decompress_dev(cfg, gath[c], ch.lay[c].msg_stride, g.P, P * n_local, ch.b0[c], ch.b1[c],
+                                         out, out_dtype, d_flags, stream))
+            return rc;
+    }
+    return TACO_OK;
 }
 
 int taco_all_gather_nccl(const taco_config* cfg, const void* x, int dtype, uint64_t n_local, void* out,
                          int out_dtype, void* work, void* comm, int* d_flags, void* stream) {
-    if (n_local == 0) return nfail(TACO_ERR_INPUT, "input tensor is empty");
-    Geo g;
-    if (int rc = comm_geo(cfg, comm, g)) return rc;
-    const uint64_t m = div_up(n_local, cfg->block_size);
-    if (int rc = taco_msg_layout(cfg, m, &g.lay)) return rc;
-    const uint64_t st = g.lay.msg_stride;
-    if (!work) return nfail(TACO_ERR_USAGE, "workspace required (taco_collective_nccl_workspace bytes)");
-    uint8_t* mine = static_cast<uint8_t*>(work);
-    uint8_t* gath = mine + st;
-    if (int rc = taco_compress_dev(cfg, x, dtype, n_local, 1, 0, m, mine, st, d_flags, stream)) return rc;
-    if (int rc = nccl_check(nccl().all_gather(mine, gath, st, ncclUint8, static_cast<ncclComm_t>(comm),
-                                              static_cast<cudaStream_t>(stream))))
-        return rc;
-    return taco_decompress_dev(cfg, gath, st, g.P, (uint64_t)g.P * n_local, 0, m, out, out_dtype, d_flags, stream);
+    return taco_all_gather_nccl_chunked(cfg, x, dtype, n_local, out, out_dtype, work, comm, d_flags, stream,
+                                        kDefaultChunks);
 }
 
 }  // extern "C"

@@ -96,3 +96,50 @@ def test_nccl_abi_errors(comm1):
     rc = lib.taco_all_gather_nccl(C.byref(bad), C.c_void_p(x.data_ptr()), 0, 1024, C.c_void_p(x.data_ptr()), 0,
                                   None, comm1, None, _st())
     assert rc == _abi.ERR_USAGE and "CodecKind::Taco" in lib.taco_last_error().decode()
+
+
+@pytest.mark.parametrize("chunks", [1, 3, 16])
+def test_nccl_abi_chunked_overlap_bit_identical_and_capturable(port, comm1, chunks):
+    """Chunked entry points (codec kernels on the caller's stream, NCCL on the library's
+    communication stream, event-ordered) equal the default chunking bit for bit, eagerly and
+    replayed from a CUDA graph of the caller's stream."""
+    n = 8192 * 40 + 3
+    cfg = make_config(256)
+    lib = _abi.lib()
+    x = torch.from_numpy(port.mixture(n, 12)).cuda().to(torch.bfloat16)
+    flags = codec.Flags()
+    dt = codec._dtype_code(torch.bfloat16)
+
+    def run(fn, ch, out, ws, nn=n):
+        args = [C.byref(cfg), C.c_void_p(x.data_ptr()), dt, nn, C.c_void_p(out.data_ptr()), _abi.DT_F32,
+                C.c_void_p(ws.data_ptr()), comm1, flags.ptr(), _st()]
+        if ch is None:
+            _abi.check(getattr(lib, fn)(*args))
+        else:
+            _abi.check(getattr(lib, fn + "_chunked")(*args, ch))
+
+    ws0 = torch.empty(lib.taco_collective_nccl_workspace(C.byref(cfg), 1, n), dtype=torch.uint8, device="cuda")
+    wsc = torch.empty(lib.taco_collective_nccl_workspace_chunked(C.byref(cfg), 1, n, chunks), dtype=torch.uint8,
+                      device="cuda")
+    for fn in ("taco_allreduce_nccl", "taco_reduce_scatter_nccl", "taco_all_gather_nccl"):
+        want = torch.empty(n, dtype=torch.float32, device="cuda")
+        got = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+        run(fn, None, want, ws0)
+        run(fn, chunks, got, wsc)
+        torch.cuda.synchronize()
+        flags.check()
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), fn
+        # captured on a side stream and replayed
+        got.fill_(float("nan"))
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            run(fn, chunks, got, wsc)
+        g.replay()
+        torch.cuda.synchronize()
+        flags.check()
+        assert torch.equal(got.view(torch.int32), want.view(torch.int32)), fn + " (graph)"
+    rc = lib.taco_allreduce_nccl_chunked(C.byref(cfg), C.c_void_p(x.data_ptr()), dt, n, C.c_void_p(x.data_ptr()),
+                                         dt, C.c_void_p(wsc.data_ptr()), comm1, None, _st(), 17)
+    assert rc == _abi.ERR_USAGE and "at most 16" in lib.taco_last_error().decode()
