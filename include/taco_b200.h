@@ -232,6 +232,38 @@ uint64_t taco_peer_flags_bytes(void);
 int taco_peer_barrier_dev(const taco_peers* peers, uint64_t flags_offset, uint32_t timeout_ms, int* d_flags,
                           void* stream);
 
+/* Fused peer collectives: the phases are signalled by the codec kernels themselves, no
+ * barrier kernels (all-reduce: 3 launches K1 -> K3 -> K2; reduce-scatter K1 -> K3 and
+ * all-gather K1 -> K2: 2).  Each kernel that reads peer-written slots first waits (thread 0
+ * of every CTA, ld.acquire.sys) until this rank's phase words reach the call's epoch; the
+ * last CTA of each writing kernel fences (fence.sc.sys after every CTA's own fence) and
+ * releases the epoch into every peer's phase word (st.release.sys).  K1 opens the epoch and
+ * first waits for the previous call's last phase, so slot reuse is safe across calls and
+ * CUDA-graph replays.  Region per rank: receive slots at recv_offset and gather slots at
+ * gath_offset (P x slot_stride each; slot [rank] is written by that rank only), the sync
+ * words at flags_offset (taco_peer_flags_bytes(); regions zeroed by taco_peer_alloc).  Do not
+ * mix fused calls and taco_peer_barrier_dev on one region.  E4M3, 64 <= B <= 512 (else
+ * TACO_ERR_USAGE: use the push kernels + barrier).  A peer that never signals raises
+ * TACO_FLAG_PEER_TIMEOUT after timeout_ms instead of hanging.  Results are bit-identical
+ * to the barrier-separated push kernels and to the NCCL transport.
+ * Reference: run_twoshot (collective.cpp:75-111) -- phase 1 exchange + owner reduce, phase 2
+ * broadcast of the re-encoded shard. */
+/* 1 when the fused peer collectives serve cfg (else use the push kernels + barrier) */
+int taco_peer_fused_supported(const taco_config* cfg);
+int taco_peer_allreduce_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                            uint64_t recv_offset, uint64_t gath_offset, uint64_t slot_stride, uint64_t flags_offset,
+                            void* out, int out_dtype, uint32_t timeout_ms, int* d_flags, void* stream);
+/* sequence-parallel reduce-scatter: x[n] -> out[ceil(n/P)] (the ascending-rank sum of this
+ * rank's shard, out_dtype) */
+int taco_peer_reduce_scatter_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
+                                 const taco_peers* peers, uint64_t recv_offset, uint64_t slot_stride,
+                                 uint64_t flags_offset, void* out, int out_dtype, uint32_t timeout_ms, int* d_flags,
+                                 void* stream);
+/* sequence-parallel all-gather: x[n_local] -> out[P * n_local] */
+int taco_peer_all_gather_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n_local,
+                             const taco_peers* peers, uint64_t gath_offset, uint64_t slot_stride, uint64_t flags_offset,
+                             void* out, int out_dtype, uint32_t timeout_ms, int* d_flags, void* stream);
+
 /* K1 into the peers: shard p's message (layout of blk_end - blk_begin blocks) goes to
  * base[p] + dst_offset + rank*slot_stride.  Taco kind, B <= 1024. */
 int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,

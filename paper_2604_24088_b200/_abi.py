@@ -119,6 +119,13 @@ _SIGNATURES = {
     "taco_allreduce_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_reduce_scatter_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_all_gather_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
+    "taco_peer_fused_supported": (C.c_int, [C.POINTER(Config)]),
+    "taco_peer_allreduce_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _U64, _U64, _U64, _U64, _P, _I, _U32,
+                                          _P, _P]),
+    "taco_peer_reduce_scatter_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _U64, _U64, _U64, _P, _I, _U32,
+                                               _P, _P]),
+    "taco_peer_all_gather_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _U64, _U64, _U64, _P, _I, _U32,
+                                           _P, _P]),
     "taco_collective_nccl_workspace_chunked": (_U64, [C.POINTER(Config), _U32, _U64, _U32]),
     "taco_allreduce_nccl_chunked": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P, _U32]),
     "taco_reduce_scatter_nccl_chunked": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P, _U32]),

@@ -251,9 +251,10 @@ uint64_t taco_archive_size(const taco_config* cfg, uint64_t n) {
 }
 
 int taco_flags_status(int flags) {
+    // a timed-out peer phase comes first: the kernels after it ran on slots that never landed
+    if (flags & TACO_FLAG_PEER_TIMEOUT) return fail(TACO_ERR_CUDA, "peer barrier timed out");
     if (flags & TACO_FLAG_NONFINITE_INPUT) return fail(TACO_ERR_INPUT, "input tensor contains NaN or Inf");
     if (flags & TACO_FLAG_BAD_SCALARS) return fail(TACO_ERR_CORRUPT, "block scalars must be finite and nonzero");
-    if (flags & TACO_FLAG_PEER_TIMEOUT) return fail(TACO_ERR_CUDA, "peer barrier timed out");
     return TACO_OK;
 }
 
@@ -382,7 +383,10 @@ int taco_peer_free(void* ptr) {
     return TACO_OK;
 }
 
-uint64_t taco_peer_flags_bytes(void) { return 4ull * TACO_MAX_PEERS + 16; }
+// barrier mode: words [0, 8) arrival slots, word 8 the epoch; fused mode (taco_peer_*_dev
+// below): the same epoch, phase-A slots words [16, 24), phase-B slots [24, 32), per-kernel
+// CTA tickets words 32..34
+uint64_t taco_peer_flags_bytes(void) { return 160; }
 
 namespace {
 int check_peers(const taco_peers* peers) {
@@ -491,6 +495,160 @@ int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64
     Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, a.dst[0], acc_out, (cudaStream_t)stream};
     if (cudaError_t e = taco_impl::launch_reduce_encode(l, a, consts_of(cfg)))
         return cuda_fail(e, "K3 reduce-encode launch");
+    return TACO_OK;
+}
+
+// ------------------------------------------------ fused peer collectives (3 / 2 launches) ---
+namespace {
+constexpr uint32_t kEpochWord = TACO_MAX_PEERS, kPhaseA = 16, kPhaseB = 24, kTicket = 32;
+
+uint32_t* flag_words(const taco_peers* peers, uint32_t q, uint64_t flags_offset) {
+    return reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(peers->base[q]) + flags_offset);
+}
+
+// wait on phase `wait_phase` of this rank's words, publish `sig_phase` into every peer's word
+// [rank] of that phase (0 = none); ticket = which kernel's CTA counter
+void set_sync(ShardArgs& a, const taco_peers* peers, uint64_t flags_offset, uint32_t wait_phase, uint32_t sig_phase,
+              bool bump, uint32_t ticket, uint32_t timeout_ms) {
+    uint32_t* own = flag_words(peers, peers->rank, flags_offset);
+    a.epoch = own + kEpochWord;
+    a.ticket = own + kTicket + ticket;
+    a.timeout_ns = (uint64_t)timeout_ms * 1000000ull;
+    if (wait_phase) {
+        a.wait_at = own + wait_phase;
+        a.nwait = peers->nranks;
+    }
+    if (sig_phase) {
+        for (uint32_t q = 0; q < peers->nranks; ++q) a.sig[q] = flag_words(peers, q, flags_offset) + sig_phase + peers->rank;
+        a.nsig = peers->nranks;
+    }
+    a.bump = bump ? 1u : 0u;
+}
+
+int check_fused(const taco_config* cfg, const taco_peers* peers, uint64_t flags_offset) {
+    if (int rc = check_push_cfg(cfg)) return rc;
+    if (int rc = check_peers(peers)) return rc;
+    if (flags_offset % 16) return fail(TACO_ERR_USAGE, "peer flag offset must be 16-byte aligned");
+    if (cfg->format != 0 || cfg->block_size < 64 || cfg->block_size > 512 || !taco_impl::xk_family())
+        return fail(TACO_ERR_USAGE, "fused peer signalling needs E4M3 and 64 <= B <= 512 "
+                                    "(use the push kernels with taco_peer_barrier_dev)");
+    return TACO_OK;
+}
+}  // namespace
+
+int taco_peer_fused_supported(const taco_config* cfg) {
+    if (check_push_cfg(cfg)) return 0;
+    return cfg->format == 0 && cfg->block_size >= 64 && cfg->block_size <= 512 && taco_impl::xk_family();
+}
+
+int taco_peer_allreduce_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n, const taco_peers* peers,
+                            uint64_t recv_offset, uint64_t gath_offset, uint64_t slot_stride, uint64_t flags_offset,
+                            void* out, int out_dtype, uint32_t timeout_ms, int* d_flags, void* stream) {
+    if (int rc = check_fused(cfg, peers, flags_offset)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_dtype(out_dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint32_t P = peers->nranks, me = peers->rank;
+    const uint64_t b = cfg->block_size, S = div_up(n, P), m = div_up(S, b);
+    const taco_layout lay = layout_of(b, m);
+    if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((recv_offset | gath_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    // K1: wait until every peer's K3 of the previous call released its receive slots (phase
+    // B), push shard p into rank p's receive slot [me], open the epoch, signal phase A
+    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a1, b);
+    for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
+    a1.ndst = P;
+    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
+    if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    // K3: wait for phase A (all P copies of my shard landed), reduce + re-encode into every
+    // rank's gather slot [me], signal phase B
+    ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, 0, d_flags};
+    taco_dev::with_full_blocks(a3, b);
+    a3.full_last = a3.full_mid;
+    for (uint32_t q = 0; q < P; ++q) a3.dst[q] = static_cast<uint8_t*>(peers->base[q]) + gath_offset + me * slot_stride;
+    a3.ndst = P;
+    set_sync(a3, peers, flags_offset, kPhaseA, kPhaseB, false, 1, timeout_ms);
+    const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
+    Launch l3{cfg->block_size, TACO_DT_F32, (int)cfg->format, own + recv_offset, a3.dst[0], nullptr, st};
+    if (cudaError_t e = taco_impl::launch_reduce_encode(l3, a3, consts_of(cfg)))
+        return cuda_fail(e, "K3 reduce-encode launch");
+    // K2: wait for phase B (every owner's re-encoded shard landed), decode locally
+    ShardArgs a2{n, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a2, b);
+    set_sync(a2, peers, flags_offset, kPhaseB, 0, false, 2, timeout_ms);
+    Launch l2{cfg->block_size, out_dtype, (int)cfg->format, own + gath_offset, out, nullptr, st};
+    if (cudaError_t e = taco_impl::launch_decompress(l2, a2, consts_of(cfg))) return cuda_fail(e, "K2 decompress launch");
+    return TACO_OK;
+}
+
+int taco_peer_reduce_scatter_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n,
+                                 const taco_peers* peers, uint64_t recv_offset, uint64_t slot_stride,
+                                 uint64_t flags_offset, void* out, int out_dtype, uint32_t timeout_ms, int* d_flags,
+                                 void* stream) {
+    if (int rc = check_fused(cfg, peers, flags_offset)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_dtype(out_dtype)) return rc;
+    if (n == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint32_t P = peers->nranks, me = peers->rank;
+    const uint64_t b = cfg->block_size, S = div_up(n, P), m = div_up(S, b);
+    const taco_layout lay = layout_of(b, m);
+    if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((recv_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+    taco_dev::with_full_blocks(a1, b);
+    for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
+    a1.ndst = P;
+    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
+    if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    // K3 with the fp32 (or bf16) stage-1 sum as the product; phase B frees the receive slots
+    ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out), d_flags};
+    taco_dev::with_full_blocks(a3, b);
+    a3.full_last = a3.full_mid;
+    set_sync(a3, peers, flags_offset, kPhaseA, kPhaseB, false, 1, timeout_ms);
+    const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
+    Launch l3{cfg->block_size, out_dtype, (int)cfg->format, own + recv_offset, nullptr, out, st};
+    if (cudaError_t e = taco_impl::launch_reduce_encode(l3, a3, consts_of(cfg)))
+        return cuda_fail(e, "K3 reduce-encode launch");
+    return TACO_OK;
+}
+
+int taco_peer_all_gather_dev(const taco_config* cfg, const void* x, int dtype, uint64_t n_local,
+                             const taco_peers* peers, uint64_t gath_offset, uint64_t slot_stride, uint64_t flags_offset,
+                             void* out, int out_dtype, uint32_t timeout_ms, int* d_flags, void* stream) {
+    if (int rc = check_fused(cfg, peers, flags_offset)) return rc;
+    if (int rc = check_dtype(dtype)) return rc;
+    if (int rc = check_dtype(out_dtype)) return rc;
+    if (n_local == 0) return fail(TACO_ERR_INPUT, "input tensor is empty");
+    const uint32_t P = peers->nranks, me = peers->rank;
+    const uint64_t b = cfg->block_size, m = div_up(n_local, b);
+    const taco_layout lay = layout_of(b, m);
+    if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
+    if ((gath_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
+    cudaStream_t st = (cudaStream_t)stream;
+    // K1 broadcast of the own slice into every rank's gather slot [me] (after every peer's
+    // K2 of the previous call released them), signal phase A
+    ShardArgs a1{n_local, n_local, 1, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x), d_flags};
+    taco_dev::with_full_blocks(a1, b);
+    for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + gath_offset + me * slot_stride;
+    a1.ndst = P;
+    a1.bcast = 1;
+    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
+    if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
+    // K2 of the P gathered slices once every rank's broadcast landed; phase B releases them
+    const uint64_t n = (uint64_t)P * n_local;
+    ShardArgs a2{n, n_local, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || n_local % 8 == 0),
+                 d_flags};
+    taco_dev::with_full_blocks(a2, b);
+    set_sync(a2, peers, flags_offset, kPhaseA, kPhaseB, false, 2, timeout_ms);
+    const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
+    Launch l2{cfg->block_size, out_dtype, (int)cfg->format, own + gath_offset, out, nullptr, st};
+    if (cudaError_t e = taco_impl::launch_decompress(l2, a2, consts_of(cfg))) return cuda_fail(e, "K2 decompress launch");
     return TACO_OK;
 }
 

@@ -49,6 +49,18 @@ struct ShardArgs {
     // buffer over NVLink) instead of msgs + r * msg_stride
     const uint8_t* src[kMaxPeers] = {};
     uint32_t nsrc = 0;
+    // fused peer signalling (taco_peer_*_dev; exchange-butterfly kernels only): before its
+    // first read a CTA waits until every word wait_at[0..nwait) of this rank's region has
+    // reached the epoch; after the last CTA's stores it publishes the epoch (bumped first
+    // when `bump`) into sig[0..nsig), one word in every peer's region (see peer_signal)
+    uint32_t* sig[kMaxPeers] = {};
+    uint32_t nsig = 0;
+    const uint32_t* wait_at = nullptr;
+    uint32_t nwait = 0;
+    uint32_t bump = 0;
+    uint32_t* epoch = nullptr;   // this rank's epoch word (own region)
+    uint32_t* ticket = nullptr;  // CTA completion count of this launch (own region, left at 0)
+    uint64_t timeout_ns = 0;
 };
 
 // programmatic dependent launch (taco_launch.h launch_k): let the next kernel on the stream
@@ -57,6 +69,67 @@ struct ShardArgs {
 __device__ __forceinline__ void grid_dep_wait() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+__device__ __forceinline__ void st_release_sys_u32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ void raise_flag(int* flags, int bit);
+
+// Peer phase wait (after grid_dep_wait, before the first read of peer-written memory):
+// thread 0 acquires every awaited word at system scope until it reaches this rank's epoch,
+// the barrier then orders the CTA's reads after it.  A peer that never signals sets
+// TACO_FLAG_PEER_TIMEOUT (4) after timeout_ns instead of hanging the stream.
+__device__ __forceinline__ void peer_wait(const ShardArgs& a) {
+    if (a.nwait == 0) return;
+    if (threadIdx.x == 0) {
+        const uint32_t e = *reinterpret_cast<volatile const uint32_t*>(a.epoch);
+        const uint64_t t0 = global_ns();
+        bool late = false;
+        for (uint32_t q = 0; q < a.nwait && !late; ++q)
+            while ((int32_t)(ld_acquire_sys_u32(a.wait_at + q) - e) < 0) {
+                if (global_ns() - t0 > a.timeout_ns) {
+                    raise_flag(a.flags, 4);
+                    late = true;
+                    break;
+                }
+                __nanosleep(100);
+            }
+    }
+    __syncthreads();
+}
+
+// Peer phase signal (every thread of every CTA, after its last store): the CTA's stores
+// (peer memory over NVLink included) are made visible system-wide by thread 0's fence
+// after the barrier, then counted; the CTA that completes the count fences again, opens
+// the next epoch if asked, and releases the epoch into every peer's signal word.  One
+// system fence per CTA (the persistent grids have a few hundred), not per thread.
+__device__ __forceinline__ void peer_signal(const ShardArgs& a) {
+    if (a.nsig == 0) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        if (atomicAdd(a.ticket, 1u) == gridDim.x * gridDim.y - 1) {
+            *reinterpret_cast<volatile uint32_t*>(a.ticket) = 0;  // the next launch counts from zero
+            __threadfence_system();
+            uint32_t e = *reinterpret_cast<volatile uint32_t*>(a.epoch);
+            if (a.bump) *reinterpret_cast<volatile uint32_t*>(a.epoch) = ++e;
+#pragma unroll
+            for (uint32_t q = 0; q < kMaxPeers; ++q)  // static indices: the parameter array stays in the constant bank
+                if (q < a.nsig) st_release_sys_u32(a.sig[q], e);
+        }
+    }
 }
 
 __device__ __forceinline__ uint8_t* shard_msg(uint8_t* msgs, const ShardArgs& a, uint64_t p) {

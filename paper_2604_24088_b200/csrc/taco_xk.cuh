@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     };
 
     grid_dep_wait();
+    if constexpr (PUSH) peer_wait(a);  // fused peer mode: the peers have finished reading the slots this K1 writes
     Tile cur{0, 0, false};
     if (t < ntiles) {
         cur = info(t);
@@ -587,6 +588,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 #endif
         cur = nxt;
     }
+    if constexpr (PUSH) peer_signal(a);
 }
 
 // --------------------------------------------------------------------- K2 --------
@@ -672,6 +674,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     };
 
     grid_dep_wait();
+    peer_wait(a);  // fused peer mode: every rank's message has landed in the gather slots
     uint32_t t = blockIdx.x * kWarps + warp;
 #pragma unroll
     for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
@@ -703,6 +706,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
         store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, a.vec_ok, w);
     }
+    peer_signal(a);
 }
 
 // --------------------------------------------------------------------- K3 --------
@@ -721,9 +725,8 @@ struct K3X {
 constexpr int kMinCtasK3 = 3;
 
 template <int L, typename TAcc>
-__global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
-    k3x(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg, TAcc* __restrict__ acc_out, ShardArgs a,
-        CodecConsts c) {
+__device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg,
+                                         TAcc* __restrict__ acc_out, const ShardArgs& a, const CodecConsts& c) {
     using K = K3X<L>;
     using D = DecPlan<L>;
     using Plan = typename D::Enc;
@@ -733,7 +736,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     uint4* stage_base = smem_dyn + (size_t)warp * K::WARP_U4;
     uint4* code_buf = stage_base + NS * K::STAGE_U4;
     const uint64_t kk0 = ((uint64_t)blockIdx.x * kWarps + warp) * G;
-    grid_dep_wait();
     if (kk0 >= a.nblk) return;  // warp-uniform
     const uint64_t kk = kk0 + g;
     const bool live = kk < a.nblk;
@@ -840,6 +842,18 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
         if (live && q == 0) *reinterpret_cast<float2*>(o + a.scal_off + kk * 8) = make_float2(alpha, s);
     }
     if (live && q == 0 && !ok) raise_flag(a.flags, 2);
+}
+
+// SYNC: the fused peer-signalling variant (taco_peer_*_dev); kept a separate instantiation
+// because the CTA-wide wait / signal costs the plain K3 ~40 bytes of register spills
+template <int L, typename TAcc, bool SYNC>
+__global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
+    k3x(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg, TAcc* __restrict__ acc_out, ShardArgs a,
+        CodecConsts c) {
+    grid_dep_wait();
+    if constexpr (SYNC) peer_wait(a);  // every rank's copy of this shard has landed
+    k3x_warp<L, TAcc>(msgs, out_msg, acc_out, a, c);
+    if constexpr (SYNC) peer_signal(a);  // ... and the re-encoded shard is in every rank's gather slot
 }
 
 }  // namespace xk

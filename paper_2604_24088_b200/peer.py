@@ -12,6 +12,12 @@ all-gather between the kernels).  Here the kernels do them with their own stores
     barrier   every K3 has landed (and nobody still reads a receive slot)
     K2        decode the P gathered shards from local memory
 
+Fused mode (the default where the exchange-butterfly kernels serve the config: E4M3,
+64 <= B <= 512): no barrier kernels.  Each kernel that reads peer-written slots waits for
+the phase words of the call's epoch itself, and the last CTA of each writing kernel
+publishes its phase (taco_peer_allreduce_dev / _reduce_scatter_dev / _all_gather_dev):
+3 launches per all-reduce (K1 -> K3 -> K2), 2 per reduce-scatter or all-gather.
+
 Each rank owns one region (CUDA-IPC exportable, include/taco_b200.h taco_peer_alloc):
 
     [ recv: P x msg_stride ][ gath: P x msg_stride ][ barrier flags ]
@@ -192,6 +198,18 @@ def _device(device):
     return torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
 
 
+def fused_supported(cfg: Config) -> bool:
+    """Whether the kernel-signalled (barrier-free) peer collectives serve cfg."""
+    return bool(_abi.lib().taco_peer_fused_supported(C.byref(cfg)))
+
+
+def _fused(cfg: Config, fused) -> bool:
+    ok = fused_supported(cfg)
+    if fused and not ok:
+        raise TacoError(_abi.ERR_USAGE, "fused peer signalling needs E4M3 and 64 <= B <= 512")
+    return ok if fused is None else bool(fused)
+
+
 class PeerTwoShotAllReduce:
     """FP8 two-shot all-reduce of a fixed-size tensor over peer memory (one process per GPU).
 
@@ -199,17 +217,21 @@ class PeerTwoShotAllReduce:
     only used once, to exchange the IPC handles of the regions."""
 
     def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
-                 device=None, timeout_ms: int = 10_000):
+                 device=None, timeout_ms: int = 10_000, fused: bool | None = None):
         self.cfg = cfg if cfg is not None else _abi.make_config()
         self.n, self.dtype = n, dtype
         self.out_dtype = out_dtype or dtype
         self.device = _device(device)
         self.timeout_ms = timeout_ms
+        self.fused = _fused(self.cfg, fused)
         self.P = dist.get_world_size(group)
         self.geo = PeerLayout(self.cfg, n, self.P)
         self.flags = Flags(self.device)
         self.map = _Mapped(self.geo.nbytes, group, self.device)
         self.peers = self.map.peers
+
+    def launches(self) -> int:
+        return 3 if self.fused else 5
 
     @property
     def shard_len(self) -> int:
@@ -218,10 +240,17 @@ class PeerTwoShotAllReduce:
     def wire_bytes_per_rank(self) -> int:
         return 2 * (self.P - 1) * self.geo.lay.msg_bytes
 
-    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         x = _input(x, self.n, self.device)
         out = _output(out, self.n, self.out_dtype, self.device)
-        push_step(self.cfg, x, self.n, self.geo, self.peers, out, self.flags, self.timeout_ms)
+        if self.fused:
+            g = self.geo
+            _abi.check(_abi.lib().taco_peer_allreduce_dev(
+                C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n, C.byref(self.peers), g.recv_off,
+                g.gath_off, g.stride, g.flags_off, _ptr(out), _dtype_code(out.dtype), self.timeout_ms,
+                self.flags.ptr(), C.c_void_p(_stream(stream))))
+        else:
+            push_step(self.cfg, x, self.n, self.geo, self.peers, out, self.flags, self.timeout_ms, stream)
         return out
 
     def check(self):
@@ -238,12 +267,13 @@ class PeerReduceScatter:
     collective.CompressedReduceScatter."""
 
     def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
-                 device=None, timeout_ms: int = 10_000):
+                 device=None, timeout_ms: int = 10_000, fused: bool | None = None):
         self.cfg = cfg if cfg is not None else _abi.make_config()
         self.n, self.dtype = n, dtype
         self.out_dtype = out_dtype or dtype
         self.device = _device(device)
         self.timeout_ms = timeout_ms
+        self.fused = _fused(self.cfg, fused)
         self.P = dist.get_world_size(group)
         self.geo = PeerLayout(self.cfg, n, self.P)
         self.flags = Flags(self.device)
@@ -261,6 +291,11 @@ class PeerReduceScatter:
         out = _output(out, self.geo.S, self.out_dtype, self.device)
         g, ps, lib = self.geo, self.map.peers, _abi.lib()
         st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
+        if self.fused:
+            _abi.check(lib.taco_peer_reduce_scatter_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n,
+                                                        C.byref(ps), g.recv_off, g.stride, g.flags_off, _ptr(out),
+                                                        _dtype_code(out.dtype), self.timeout_ms, fl, st))
+            return out
         _abi.check(lib.taco_compress_push_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n, C.byref(ps),
                                               0, g.m, g.recv_off, g.stride, fl, st))
         _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), g.flags_off, self.timeout_ms, fl, st))
@@ -282,12 +317,13 @@ class PeerAllGather:
     barrier (the gather slots are free again).  Bit-identical to collective.CompressedAllGather."""
 
     def __init__(self, n_local: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
-                 device=None, timeout_ms: int = 10_000):
+                 device=None, timeout_ms: int = 10_000, fused: bool | None = None):
         self.cfg = cfg if cfg is not None else _abi.make_config()
         self.n_local = n_local
         self.out_dtype = out_dtype or dtype
         self.device = _device(device)
         self.timeout_ms = timeout_ms
+        self.fused = _fused(self.cfg, fused)
         self.P = dist.get_world_size(group)
         self.m = cdiv(n_local, self.cfg.block_size)
         self.lay = _abi.msg_layout(self.cfg, self.m)
@@ -305,6 +341,11 @@ class PeerAllGather:
         out = _output(out, n, self.out_dtype, self.device)
         ps, lib = self.map.peers, _abi.lib()
         st, fl = C.c_void_p(_stream(stream)), self.flags.ptr()
+        if self.fused:
+            _abi.check(lib.taco_peer_all_gather_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n_local,
+                                                    C.byref(ps), 0, self.stride, self.flags_off, _ptr(out),
+                                                    _dtype_code(out.dtype), self.timeout_ms, fl, st))
+            return out
         _abi.check(lib.taco_compress_bcast_dev(C.byref(self.cfg), _ptr(x), _dtype_code(x.dtype), self.n_local,
                                                C.byref(ps), 0, self.m, 0, self.stride, fl, st))
         _abi.check(lib.taco_peer_barrier_dev(C.byref(ps), self.flags_off, self.timeout_ms, fl, st))

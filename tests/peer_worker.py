@@ -1,5 +1,6 @@
 """Worker of tests/test_gpu_peer.py: P processes sharing ONE GPU run the peer-memory
-two-shot (CUDA IPC between processes, device barriers, K1/K3 pushes) and check every
+two-shot (CUDA IPC between processes, device barriers or the kernels' own phase signals,
+K1/K3 pushes) and check every
 result bit-for-bit against the one-process simulation of the same schedule.
 
 Launched by torch.distributed.run; gloo only exchanges the IPC handles.  Prints
@@ -25,13 +26,15 @@ def inputs_for(world, n, dtype, seed):
 
 def main():
     n, b, dt = int(sys.argv[1]), int(sys.argv[2]), sys.argv[3]
+    fused = bool(int(sys.argv[4])) if len(sys.argv) > 4 else None
     dtype = torch.bfloat16 if dt == "bf16" else torch.float32
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
     cfg = make_config(b)
     ar = peer.PeerTwoShotAllReduce(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0",
-                                   timeout_ms=30_000)
+                                   timeout_ms=30_000, fused=fused)
+    assert fused is None or ar.fused == fused
     # eager calls with fresh inputs every time (stale slots would show up as mismatches)
     for it in range(3):
         ins = inputs_for(world, n, dtype, 1000 + it)
@@ -60,8 +63,10 @@ def main():
     ar.close()
     # sequence-parallel pair: reduce-scatter (fp32 stage-1 sums) and all-gather
     S = -(-n // world)
-    rs = peer.PeerReduceScatter(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000)
-    ag = peer.PeerAllGather(S, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000)
+    rs = peer.PeerReduceScatter(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000,
+                                fused=fused)
+    ag = peer.PeerAllGather(S, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000,
+                            fused=fused)
     for it in range(2):
         ins = inputs_for(world, n, dtype, 3000 + it)
         stage1 = torch.empty(world * S, dtype=torch.float32, device="cuda")
@@ -79,7 +84,7 @@ def main():
     rs.close()
     ag.close()
     dist.destroy_process_group()
-    print(f"PEER_OK {rank}", flush=True)
+    print(f"PEER_OK {rank} fused={int(ar.fused)}", flush=True)
 
 
 if __name__ == "__main__":

@@ -88,16 +88,113 @@ def _free_port():
     return port
 
 
-@pytest.mark.parametrize("procs,n,b,dt", [(2, 8192 * 24, 256, "bf16"), (3, 30_001, 128, "f32")])
-def test_peer_allreduce_processes_share_one_gpu(procs, n, b, dt):
+@pytest.mark.parametrize("procs,n,b,dt,fused", [(2, 8192 * 24, 256, "bf16", 1), (3, 30_001, 128, "f32", 1),
+                                                (2, 8192 * 24, 256, "bf16", 0), (3, 30_001, 32, "f32", 0)])
+def test_peer_allreduce_processes_share_one_gpu(procs, n, b, dt, fused):
+    """fused = 1: the kernels signal the phases themselves (3 launches per all-reduce);
+    fused = 0: the push kernels with barrier kernels between the phases (5 launches)."""
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={procs}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
-           os.path.join(ROOT, "tests", "peer_worker.py"), str(n), str(b), dt]
+           os.path.join(ROOT, "tests", "peer_worker.py"), str(n), str(b), dt, str(fused)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     tail = (r.stdout[-3000:] + r.stderr[-3000:])
     assert r.returncode == 0, tail
     for rank in range(procs):
-        assert f"PEER_OK {rank}" in r.stdout, tail
+        assert f"PEER_OK {rank} fused={fused}" in r.stdout, tail
+
+
+def _fused_call(kind, cfg, x, n, ps, geo, out, flags, timeout_ms=10_000):
+    import ctypes as C
+    lib, st = _abi.lib(), C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    dt = codec._dtype_code
+    if kind == "ar":
+        return lib.taco_peer_allreduce_dev(C.byref(cfg), C.c_void_p(x.data_ptr()), dt(x.dtype), n, C.byref(ps),
+                                           geo.recv_off, geo.gath_off, geo.stride, geo.flags_off,
+                                           C.c_void_p(out.data_ptr()), dt(out.dtype), timeout_ms, flags.ptr(), st)
+    return lib.taco_peer_reduce_scatter_dev(C.byref(cfg), C.c_void_p(x.data_ptr()), dt(x.dtype), n, C.byref(ps),
+                                            geo.recv_off, geo.stride, geo.flags_off, C.c_void_p(out.data_ptr()),
+                                            dt(out.dtype), timeout_ms, flags.ptr(), st)
+
+
+@pytest.mark.parametrize("b,dtype", [(256, torch.bfloat16), (64, torch.float32), (512, torch.bfloat16)])
+def test_fused_peer_group_of_one_matches_and_keeps_counting(b, dtype):
+    """A group of one: the fused kernels wait on and signal their own words.  Repeated calls
+    and CUDA-graph replays keep the epoch counting; the result equals the barrier path."""
+    cfg = make_config(b)
+    n = 8192 * 5 + 7
+    geo = peer.PeerLayout(cfg, n, 1)
+    dev = torch.cuda.current_device()
+    reg = peer.PeerRegion(geo.nbytes, dev)
+    try:
+        ps = peer.peers_struct([reg.ptr], 0)
+        flags = codec.Flags()
+        x = _inputs(1, n, dtype, 5)[0]
+        want = peer.allreduce_sim_peer(x[None], cfg)[0]
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            out.fill_(float("nan"))
+            _abi.check(_fused_call("ar", cfg, x, n, ps, geo, out, flags))
+            torch.cuda.synchronize()
+            flags.check()
+            assert torch.equal(out.view(torch.int32), want.view(torch.int32))
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            _abi.check(_fused_call("ar", cfg, x, n, ps, geo, out, flags))
+        for _ in range(3):
+            out.fill_(float("nan"))
+            g.replay()
+            torch.cuda.synchronize()
+            flags.check()
+            assert torch.equal(out.view(torch.int32), want.view(torch.int32))
+        # reduce-scatter of one rank: the stage-1 sum == a K2 decode of K1's message
+        rs = torch.empty(n, dtype=torch.float32, device="cuda")
+        _abi.check(_fused_call("rs", cfg, x, n, ps, geo, rs, flags))
+        torch.cuda.synchronize()
+        flags.check()
+        assert torch.equal(rs, codec.decompress(codec.compress(x, cfg), n, cfg))
+    finally:
+        torch.cuda.synchronize()
+        reg.free()
+
+
+def test_fused_peer_times_out_instead_of_hanging():
+    """Rank 1 never runs: rank 0's K3 and K2 give up after the timeout and raise the flag."""
+    cfg = make_config(256)
+    n = 4096 * 8
+    geo = peer.PeerLayout(cfg, n, 2)
+    dev = torch.cuda.current_device()
+    a, b = peer.PeerRegion(geo.nbytes, dev), peer.PeerRegion(geo.nbytes, dev)
+    try:
+        ps = peer.peers_struct([a.ptr, b.ptr], 0)
+        flags = codec.Flags()
+        x = _inputs(1, n, torch.bfloat16, 6)[0]
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        _abi.check(_fused_call("ar", cfg, x, n, ps, geo, out, flags, timeout_ms=200))
+        torch.cuda.synchronize()
+        with pytest.raises(TacoError, match="peer barrier timed out"):
+            flags.check()
+    finally:
+        torch.cuda.synchronize()
+        a.free()
+        b.free()
+
+
+def test_fused_peer_rejects_unserved_configs():
+    import ctypes as C
+    assert peer.fused_supported(make_config(256)) and not peer.fused_supported(make_config(256, 1))
+    assert not peer.fused_supported(make_config(1024)) and not peer.fused_supported(make_config(32))
+    cfg = make_config(1024)
+    geo = peer.PeerLayout(cfg, 4096, 1)
+    reg = peer.PeerRegion(geo.nbytes, torch.cuda.current_device())
+    try:
+        ps = peer.peers_struct([reg.ptr], 0)
+        x = torch.zeros(4096, device="cuda")
+        rc = _fused_call("ar", cfg, x, 4096, ps, geo, x, codec.Flags())
+        assert rc == _abi.ERR_USAGE and "fused peer signalling" in _abi.lib().taco_last_error().decode()
+    finally:
+        reg.free()
 
 
 def test_peer_barrier_times_out_instead_of_hanging():
