@@ -576,6 +576,8 @@ def main():
     ap.add_argument("--size-sweep", type=lambda t: [float(v) for v in t.split(",")] if t else [], default=None,
                     help="N>1: configs[4] message sizes in MB (default 1,16,256 at N>1; empty string disables)")
     ap.add_argument("--collective", action="store_true", help="run the collective leg even at world size 1")
+    ap.add_argument("--plan", action="store_true",
+                    help="N>1: print what this N measures (workload, legs, NCCL comparators) without a GPU")
     ap.add_argument("--config", type=int, choices=sorted(CONFIGS), default=None,
                     help="BASELINE.json configs index of the per-rank tensor (N=1 default: 3, the largest; "
                          "N>1 default: 1 / 2 / 3 at 2 / 4 / 8 GPUs)")
@@ -597,6 +599,17 @@ def main():
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args, n_ranks)), flush=True)
+        return
+    if args.plan:
+        from bench_collective import plan
+        if world > 1:
+            import torch.distributed as dist
+            dist.init_process_group("gloo")  # the launch plumbing the real run uses
+            dist.barrier()
+        if rank == 0:
+            print(json.dumps(plan(args, max(world, args.gpus))), flush=True)
+        if world > 1:
+            dist.destroy_process_group()
         return
     if world > 1 or args.collective:
         from bench_collective import run_collective

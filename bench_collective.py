@@ -136,7 +136,8 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
     return {"ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
             "speedup_vs_nccl_twoshot": round(step_ms / ms, 3),
             "bit_identical_to_nccl_twoshot": bool(int(t[0].item()) == 1),
-            "gpu_launches_per_step": 5, "barriers_per_step": 2}
+            "fused_signalling": par.fused, "gpu_launches_per_step": par.launches(),
+            "barrier_kernels_per_step": 0 if par.fused else 2}
 
 
 def _sp_leg(args, n, cfg, xs, stream, use_graphs, peer_leg=True):
@@ -306,6 +307,27 @@ def _ar_leg(args, n, cfg, xs, outs, stream, chunks):
         "speedup_vs_nccl_bf16": round(nccl_ms / ms, 3),
         "wire_bytes_per_rank": wire, "wire_frac_of_nvlink_900": round(wire / (ms * 1e-3) / 900e9, 4),
         "chunks": chunks, "launch": note}
+
+
+def plan(args, world: int) -> dict:
+    """What `bench.py --gpus N` measures at this N, without touching a GPU (`--plan`): the
+    workload, every leg and both bf16 NCCL comparators."""
+    idx = args.config
+    legs = ["fp8_twoshot_allreduce (NCCL transport, chunked, CUDA graph)", "peer_memory_twoshot (fused signalling)"]
+    if idx == 2 or args.collective:
+        legs += ["sequence_parallel reduce-scatter + all-gather (NCCL and peer transports)",
+                 "sequence_parallel_block_sweep B in " + ",".join(str(b) for b in args.block_sweep)]
+    if idx == 3 or args.collective:
+        legs += ["backward_gradient_allreduce (x 2^-6 activation-gradients)"]
+    if args.size_sweep:
+        legs += ["message_size_sweep " + ",".join(f"{mb}MB" for mb in args.size_sweep)]
+    return {"plan": True, "n_gpus": world, "config": workload_config(args, world), "legs": legs,
+            "nccl_bf16_comparators": [
+                {"what": "ncclAllReduce / reduce_scatter_tensor / all_gather_into_tensor bf16, same tensors",
+                 "NCCL_NVLS_ENABLE": os.environ.get("NCCL_NVLS_ENABLE", "default") if args.nccl_nvls is None
+                 else str(args.nccl_nvls)},
+                {"what": "the same with NVLink SHARP off", "run": "bench.py --gpus N --nccl-nvls 0"}],
+            "nccl_record": "version, NVLS availability and toggles from the NCCL INIT log (NCCL_DEBUG_FILE)"}
 
 
 def run_collective(args, rows, cols, clock_sampler, peaks):

@@ -220,6 +220,10 @@ int taco_peer_alloc(int device, uint64_t bytes, void** ptr, taco_ipc_handle* han
 /* map a peer's exported region into this process (on `device`, this rank's GPU) */
 int taco_peer_open(int device, const taco_ipc_handle* handle, void** ptr);
 int taco_peer_close(void* ptr);
+/* TACO_OK when `device` can map memory of `peer_device` (cudaDeviceCanAccessPeer; the same
+ * device always can); else TACO_ERR_USAGE naming both.  The opened mappings enable peer
+ * access lazily (cudaIpcMemLazyEnablePeerAccess). */
+int taco_peer_check_access(int device, int peer_device);
 int taco_peer_free(void* ptr);
 /* bytes of the barrier state at flags_offset: P arrival slots + this rank's epoch */
 uint64_t taco_peer_flags_bytes(void);

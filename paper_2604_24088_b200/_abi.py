@@ -120,6 +120,7 @@ _SIGNATURES = {
     "taco_reduce_scatter_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_all_gather_nccl": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _I, _P, _P, _P, _P]),
     "taco_peer_fused_supported": (C.c_int, [C.POINTER(Config)]),
+    "taco_peer_check_access": (C.c_int, [C.c_int, C.c_int]),
     "taco_peer_allreduce_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _U64, _U64, _U64, _U64, _P, _I, _U32,
                                           _P, _P]),
     "taco_peer_reduce_scatter_dev": (C.c_int, [C.POINTER(Config), _P, _I, _U64, _P, _U64, _U64, _U64, _P, _I, _U32,

@@ -373,6 +373,16 @@ int taco_peer_open(int device, const taco_ipc_handle* handle, void** ptr) {
     return TACO_OK;
 }
 
+int taco_peer_check_access(int device, int peer_device) {
+    if (device == peer_device) return TACO_OK;  // processes sharing one GPU: IPC within the device
+    int can = 0;
+    TACO_CUDA(cudaDeviceCanAccessPeer(&can, device, peer_device));
+    if (!can)
+        return fail(TACO_ERR_USAGE, "no peer-to-peer path from GPU " + std::to_string(device) + " to GPU " +
+                                        std::to_string(peer_device) + " (NVLink / PCIe P2P unavailable)");
+    return TACO_OK;
+}
+
 int taco_peer_close(void* ptr) {
     TACO_CUDA(cudaIpcCloseMemHandle(ptr));
     return TACO_OK;

@@ -131,15 +131,18 @@ class _Mapped:
         dix = device.index if device.index is not None else torch.cuda.current_device()
         self.region = PeerRegion(nbytes, dix)
         handles = [None] * self.P
-        dist.all_gather_object(handles, self.region.handle_bytes(), group=group)
+        dist.all_gather_object(handles, (self.region.handle_bytes(), dix), group=group)
+        self.devices = [d for _, d in handles]
         self.bases, self.opened = [], []
         err = ""
         try:
             for q in range(self.P):
+                _abi.check(_abi.lib().taco_peer_check_access(dix, self.devices[q]))
+            for q in range(self.P):
                 if q == self.rank:
                     self.bases.append(self.region.ptr)
                 else:
-                    p = open_handle(handles[q], dix)
+                    p = open_handle(handles[q][0], dix)
                     self.opened.append(p)
                     self.bases.append(p)
         except TacoError as e:  # e.g. no P2P path between two GPUs

@@ -30,9 +30,11 @@ def main():
     dtype = torch.bfloat16 if dt == "bf16" else torch.float32
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
-    torch.cuda.set_device(0)
+    # one GPU per rank when the box has enough (real NVLink peers), else all ranks share GPU 0
+    dev = int(os.environ.get("LOCAL_RANK", rank)) % torch.cuda.device_count()
+    torch.cuda.set_device(dev)
     cfg = make_config(b)
-    ar = peer.PeerTwoShotAllReduce(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0",
+    ar = peer.PeerTwoShotAllReduce(n, cfg, dtype=dtype, out_dtype=torch.float32, device=f"cuda:{dev}",
                                    timeout_ms=30_000, fused=fused)
     assert fused is None or ar.fused == fused
     # eager calls with fresh inputs every time (stale slots would show up as mismatches)
@@ -63,9 +65,9 @@ def main():
     ar.close()
     # sequence-parallel pair: reduce-scatter (fp32 stage-1 sums) and all-gather
     S = -(-n // world)
-    rs = peer.PeerReduceScatter(n, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000,
+    rs = peer.PeerReduceScatter(n, cfg, dtype=dtype, out_dtype=torch.float32, device=f"cuda:{dev}", timeout_ms=30_000,
                                 fused=fused)
-    ag = peer.PeerAllGather(S, cfg, dtype=dtype, out_dtype=torch.float32, device="cuda:0", timeout_ms=30_000,
+    ag = peer.PeerAllGather(S, cfg, dtype=dtype, out_dtype=torch.float32, device=f"cuda:{dev}", timeout_ms=30_000,
                             fused=fused)
     for it in range(2):
         ins = inputs_for(world, n, dtype, 3000 + it)
