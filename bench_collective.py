@@ -223,12 +223,16 @@ def _sp_leg(args, n, cfg, xs, stream, use_graphs, peer_leg=True):
 
 
 def _nccl_logging() -> str | None:
-    """NCCL INIT lines go to a per-process file (and stay out of rank 0's stdout, which is
-    the one JSON line); returns the file name, read back for the algorithm record."""
-    if "NCCL_DEBUG" in os.environ:
-        return os.environ.get("NCCL_DEBUG_FILE")
+    """NCCL's log lines (INIT, and the version banner NCCL_DEBUG=VERSION prints) go to a
+    per-process file and never to rank 0's stdout, which is the one JSON line; returns the
+    file name, read back for the algorithm record."""
+    if os.environ.get("NCCL_DEBUG_FILE"):
+        return os.environ["NCCL_DEBUG_FILE"]
     path = f"/tmp/taco_nccl_init.{os.getpid()}.log"
-    os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,ENV", NCCL_DEBUG_FILE=path)
+    level = os.environ.get("NCCL_DEBUG", "").upper()
+    if level not in ("INFO", "TRACE"):
+        os.environ.update(NCCL_DEBUG="INFO", NCCL_DEBUG_SUBSYS="INIT,ENV")
+    os.environ["NCCL_DEBUG_FILE"] = path
     return path
 
 

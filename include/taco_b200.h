@@ -238,18 +238,20 @@ int taco_peer_barrier_dev(const taco_peers* peers, uint64_t flags_offset, uint32
 
 /* Fused peer collectives: the phases are signalled by the codec kernels themselves, no
  * barrier kernels (all-reduce: 3 launches K1 -> K3 -> K2; reduce-scatter K1 -> K3 and
- * all-gather K1 -> K2: 2).  Each kernel that reads peer-written slots first waits (thread 0
- * of every CTA, ld.acquire.sys) until this rank's phase words reach the call's epoch; the
- * last CTA of each writing kernel fences (fence.sc.sys after every CTA's own fence) and
- * releases the epoch into every peer's phase word (st.release.sys).  K1 opens the epoch and
- * first waits for the previous call's last phase, so slot reuse is safe across calls and
- * CUDA-graph replays.  Region per rank: receive slots at recv_offset and gather slots at
- * gath_offset (P x slot_stride each; slot [rank] is written by that rank only), the sync
- * words at flags_offset (taco_peer_flags_bytes(); regions zeroed by taco_peer_alloc).  Do not
- * mix fused calls and taco_peer_barrier_dev on one region.  E4M3, 64 <= B <= 512 (else
- * TACO_ERR_USAGE: use the push kernels + barrier).  A peer that never signals raises
- * TACO_FLAG_PEER_TIMEOUT after timeout_ms instead of hanging.  Results are bit-identical
- * to the barrier-separated push kernels and to the NCCL transport.
+ * all-gather K1 -> K2: 2).  K1's last CTA fences (fence.sc.sys after every CTA's GPU-scope
+ * release), opens the call's epoch, releases it into every peer's phase-A word
+ * (st.release.sys) and waits (ld.acquire.sys) for every peer's: K1 completes only when every
+ * rank's pushes have landed, so K3 runs unmodified.  In the all-reduce, K2's CTA 0 publishes
+ * phase B (this rank's K3 is done) and every K2 CTA waits for all peers' before decoding;
+ * the reduce-scatter / all-gather K1 starts with phase B instead (the previous call's K3 / K2
+ * is done with the slots).  Slot reuse is therefore safe across calls and CUDA-graph replays.
+ * Region per rank: receive slots at recv_offset and gather slots at gath_offset (P x
+ * slot_stride each; slot [rank] is written by that rank only), the sync words at flags_offset
+ * (taco_peer_flags_bytes(); regions zeroed by taco_peer_alloc).  Do not mix fused calls and
+ * taco_peer_barrier_dev on one region.  E4M3, 64 <= B <= 512 (else TACO_ERR_USAGE: use the
+ * push kernels + barrier).  A peer that never signals raises TACO_FLAG_PEER_TIMEOUT after
+ * timeout_ms instead of hanging.  Results are bit-identical to the barrier-separated push
+ * kernels and to the NCCL transport.
  * Reference: run_twoshot (collective.cpp:75-111) -- phase 1 exchange + owner reduce, phase 2
  * broadcast of the re-encoded shard. */
 /* 1 when the fused peer collectives serve cfg (else use the push kernels + barrier) */

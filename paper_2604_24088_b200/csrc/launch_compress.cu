@@ -100,7 +100,7 @@ cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0 || a.P == 0) return cudaSuccess;
-    if (a.nsig | a.nwait) {  // fused peer signalling lives in the exchange-butterfly kernels only
+    if (a.npre | a.npost) {  // the fused peer phases live in the exchange-butterfly K1 / K2 only
         if constexpr (!(FMT == 0 && B >= 64 && B <= 512)) return cudaErrorNotSupported;
         if (!xk_family() || a.nblk >= (1ull << 31)) return cudaErrorNotSupported;
     }

@@ -11,7 +11,7 @@ namespace {
 template <int L, typename T>
 cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     using K = xk::K3X<L>;
-    auto* kern = (a.nsig | a.nwait) ? &xk::k3x<L, T, true> : &xk::k3x<L, T, false>;
+    auto* kern = &xk::k3x<L, T>;
     const uint64_t tiles = (a.nblk + K::G - 1) / K::G;
     const unsigned grid = (unsigned)((tiles + xk::kWarps - 1) / xk::kWarps);
     return launch_k(kern, grid, xk::kWarps * 32, K::SMEM, l.stream, static_cast<const uint8_t*>(l.in),
@@ -21,7 +21,7 @@ cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
 template <int B, typename T, int FMT>
 cudaError_t run(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     if (a.nblk == 0) return cudaSuccess;
-    if (a.nsig | a.nwait) {  // fused peer signalling lives in the exchange-butterfly kernels only
+    if (a.npre | a.npost) {  // the fused peer phases live in the exchange-butterfly K1 / K2 only (K3 is plain)
         if constexpr (!(FMT == 0 && B >= 64 && B <= 512)) return cudaErrorNotSupported;
         if (!xk_family() || a.nblk >= (1ull << 31)) return cudaErrorNotSupported;
     }

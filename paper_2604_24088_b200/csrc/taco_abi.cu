@@ -516,23 +516,33 @@ uint32_t* flag_words(const taco_peers* peers, uint32_t q, uint64_t flags_offset)
     return reinterpret_cast<uint32_t*>(static_cast<uint8_t*>(peers->base[q]) + flags_offset);
 }
 
-// wait on phase `wait_phase` of this rank's words, publish `sig_phase` into every peer's word
-// [rank] of that phase (0 = none); ticket = which kernel's CTA counter
-void set_sync(ShardArgs& a, const taco_peers* peers, uint64_t flags_offset, uint32_t wait_phase, uint32_t sig_phase,
-              bool bump, uint32_t ticket, uint32_t timeout_ms) {
+// this rank's words of `phase` in its own region, and its word [rank] of that phase in
+// every peer's region
+void phase_words(const taco_peers* peers, uint64_t flags_offset, uint32_t phase, const uint32_t*& own,
+                 uint32_t* (&at_peers)[taco_dev::kMaxPeers]) {
+    own = flag_words(peers, peers->rank, flags_offset) + phase;
+    for (uint32_t q = 0; q < peers->nranks; ++q) at_peers[q] = flag_words(peers, q, flags_offset) + phase + peers->rank;
+}
+
+void set_common(ShardArgs& a, const taco_peers* peers, uint64_t flags_offset, uint32_t timeout_ms) {
     uint32_t* own = flag_words(peers, peers->rank, flags_offset);
     a.epoch = own + kEpochWord;
-    a.ticket = own + kTicket + ticket;
+    a.ticket = own + kTicket;
     a.timeout_ns = (uint64_t)timeout_ms * 1000000ull;
-    if (wait_phase) {
-        a.wait_at = own + wait_phase;
-        a.nwait = peers->nranks;
-    }
-    if (sig_phase) {
-        for (uint32_t q = 0; q < peers->nranks; ++q) a.sig[q] = flag_words(peers, q, flags_offset) + sig_phase + peers->rank;
-        a.nsig = peers->nranks;
-    }
-    a.bump = bump ? 1u : 0u;
+}
+
+// kernel start: publish "done with the slots" for `phase`, wait for every peer's
+void set_pre(ShardArgs& a, const taco_peers* peers, uint64_t flags_offset, uint32_t phase, uint32_t timeout_ms) {
+    set_common(a, peers, flags_offset, timeout_ms);
+    phase_words(peers, flags_offset, phase, a.pre_wait, a.pre_sig);
+    a.npre = peers->nranks;
+}
+
+// kernel end: the last CTA opens the next epoch, publishes `phase`, waits for every peer's
+void set_post(ShardArgs& a, const taco_peers* peers, uint64_t flags_offset, uint32_t phase, uint32_t timeout_ms) {
+    set_common(a, peers, flags_offset, timeout_ms);
+    phase_words(peers, flags_offset, phase, a.post_wait, a.post_sig);
+    a.npost = peers->nranks;
 }
 
 int check_fused(const taco_config* cfg, const taco_peers* peers, uint64_t flags_offset) {
@@ -564,31 +574,30 @@ int taco_peer_allreduce_dev(const taco_config* cfg, const void* x, int dtype, ui
     if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((recv_offset | gath_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
-    // K1: wait until every peer's K3 of the previous call released its receive slots (phase
-    // B), push shard p into rank p's receive slot [me], open the epoch, signal phase A
+    // K1: push shard p into rank p's receive slot [me]; its last CTA opens the epoch,
+    // publishes phase A and waits for every peer's (all P copies of my shard have landed)
     ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
     a1.ndst = P;
-    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    set_post(a1, peers, flags_offset, kPhaseA, timeout_ms);
     Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
     if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
-    // K3: wait for phase A (all P copies of my shard landed), reduce + re-encode into every
-    // rank's gather slot [me], signal phase B
+    // K3 (plain): reduce + re-encode into every rank's gather slot [me]
     ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, 0, d_flags};
     taco_dev::with_full_blocks(a3, b);
     a3.full_last = a3.full_mid;
     for (uint32_t q = 0; q < P; ++q) a3.dst[q] = static_cast<uint8_t*>(peers->base[q]) + gath_offset + me * slot_stride;
     a3.ndst = P;
-    set_sync(a3, peers, flags_offset, kPhaseA, kPhaseB, false, 1, timeout_ms);
     const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
     Launch l3{cfg->block_size, TACO_DT_F32, (int)cfg->format, own + recv_offset, a3.dst[0], nullptr, st};
     if (cudaError_t e = taco_impl::launch_reduce_encode(l3, a3, consts_of(cfg)))
         return cuda_fail(e, "K3 reduce-encode launch");
-    // K2: wait for phase B (every owner's re-encoded shard landed), decode locally
+    // K2: publish phase B (my K3 is done: my receive slots are free, my gather pushes are
+    // out), wait for every peer's, decode locally
     ShardArgs a2{n, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || S % 8 == 0), d_flags};
     taco_dev::with_full_blocks(a2, b);
-    set_sync(a2, peers, flags_offset, kPhaseB, 0, false, 2, timeout_ms);
+    set_pre(a2, peers, flags_offset, kPhaseB, timeout_ms);
     Launch l2{cfg->block_size, out_dtype, (int)cfg->format, own + gath_offset, out, nullptr, st};
     if (cudaError_t e = taco_impl::launch_decompress(l2, a2, consts_of(cfg))) return cuda_fail(e, "K2 decompress launch");
     return TACO_OK;
@@ -612,14 +621,16 @@ int taco_peer_reduce_scatter_dev(const taco_config* cfg, const void* x, int dtyp
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
     a1.ndst = P;
-    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    // K1: phase B first (my previous K3 is done with my receive slots; wait until every
+    // peer's is), push, then phase A (every rank's pushes have landed)
+    set_pre(a1, peers, flags_offset, kPhaseB, timeout_ms);
+    set_post(a1, peers, flags_offset, kPhaseA, timeout_ms);
     Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
     if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
-    // K3 with the fp32 (or bf16) stage-1 sum as the product; phase B frees the receive slots
+    // K3 (plain) with the fp32 (or bf16) stage-1 sum as the product
     ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out), d_flags};
     taco_dev::with_full_blocks(a3, b);
     a3.full_last = a3.full_mid;
-    set_sync(a3, peers, flags_offset, kPhaseA, kPhaseB, false, 1, timeout_ms);
     const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
     Launch l3{cfg->block_size, out_dtype, (int)cfg->format, own + recv_offset, nullptr, out, st};
     if (cudaError_t e = taco_impl::launch_reduce_encode(l3, a3, consts_of(cfg)))
@@ -640,22 +651,23 @@ int taco_peer_all_gather_dev(const taco_config* cfg, const void* x, int dtype, u
     if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((gath_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
-    // K1 broadcast of the own slice into every rank's gather slot [me] (after every peer's
-    // K2 of the previous call released them), signal phase A
+    // K1 broadcast of the own slice into every rank's gather slot [me]: phase B first (every
+    // peer's K2 of the previous call is done with the gather slots), then phase A (every
+    // rank's broadcast has landed)
     ShardArgs a1{n_local, n_local, 1, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x), d_flags};
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + gath_offset + me * slot_stride;
     a1.ndst = P;
     a1.bcast = 1;
-    set_sync(a1, peers, flags_offset, kPhaseB, kPhaseA, true, 0, timeout_ms);
+    set_pre(a1, peers, flags_offset, kPhaseB, timeout_ms);
+    set_post(a1, peers, flags_offset, kPhaseA, timeout_ms);
     Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
     if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
-    // K2 of the P gathered slices once every rank's broadcast landed; phase B releases them
+    // K2 (plain) of the P gathered slices
     const uint64_t n = (uint64_t)P * n_local;
     ShardArgs a2{n, n_local, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || n_local % 8 == 0),
                  d_flags};
     taco_dev::with_full_blocks(a2, b);
-    set_sync(a2, peers, flags_offset, kPhaseA, kPhaseB, false, 2, timeout_ms);
     const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
     Launch l2{cfg->block_size, out_dtype, (int)cfg->format, own + gath_offset, out, nullptr, st};
     if (cudaError_t e = taco_impl::launch_decompress(l2, a2, consts_of(cfg))) return cuda_fail(e, "K2 decompress launch");

@@ -49,15 +49,19 @@ struct ShardArgs {
     // buffer over NVLink) instead of msgs + r * msg_stride
     const uint8_t* src[kMaxPeers] = {};
     uint32_t nsrc = 0;
-    // fused peer signalling (taco_peer_*_dev; exchange-butterfly kernels only): before its
-    // first read a CTA waits until every word wait_at[0..nwait) of this rank's region has
-    // reached the epoch; after the last CTA's stores it publishes the epoch (bumped first
-    // when `bump`) into sig[0..nsig), one word in every peer's region (see peer_signal)
-    uint32_t* sig[kMaxPeers] = {};
-    uint32_t nsig = 0;
-    const uint32_t* wait_at = nullptr;
-    uint32_t nwait = 0;
-    uint32_t bump = 0;
+    // fused peer signalling (taco_peer_*_dev; the exchange-butterfly K1 / K2 only, K3 stays
+    // plain).  "pre" (kernel start, after grid_dep_wait): CTA 0 publishes this rank's epoch
+    // into pre_sig[0..npre) -- one word per peer, "the kernels before this one are done with
+    // the slots" -- then every CTA waits until this rank's words pre_wait[0..npre) reach it.
+    // "post" (kernel end): the last CTA to finish opens the next epoch, publishes it into
+    // post_sig[0..npost) and waits until post_wait[0..npost) reach it, so the next kernel on
+    // the stream only reads slots every peer has finished writing (peer_pre / peer_post).
+    uint32_t* pre_sig[kMaxPeers] = {};
+    const uint32_t* pre_wait = nullptr;
+    uint32_t npre = 0;
+    uint32_t* post_sig[kMaxPeers] = {};
+    const uint32_t* post_wait = nullptr;
+    uint32_t npost = 0;
     uint32_t* epoch = nullptr;   // this rank's epoch word (own region)
     uint32_t* ticket = nullptr;  // CTA completion count of this launch (own region, left at 0)
     uint64_t timeout_ns = 0;
@@ -87,47 +91,64 @@ __device__ __forceinline__ uint64_t global_ns() {
 
 __device__ __forceinline__ void raise_flag(int* flags, int bit);
 
-// Peer phase wait (after grid_dep_wait, before the first read of peer-written memory):
-// thread 0 acquires every awaited word at system scope until it reaches this rank's epoch,
-// the barrier then orders the CTA's reads after it.  A peer that never signals sets
-// TACO_FLAG_PEER_TIMEOUT (4) after timeout_ns instead of hanging the stream.
-__device__ __forceinline__ void peer_wait(const ShardArgs& a) {
-    if (a.nwait == 0) return;
+// Thread-local poll of n words of this rank's region until each reaches e (system-scope
+// acquire).  A peer that never signals sets TACO_FLAG_PEER_TIMEOUT (4) after timeout_ns
+// instead of hanging the stream.
+__device__ __forceinline__ void wait_words(const uint32_t* w, uint32_t n, uint32_t e, uint64_t timeout_ns,
+                                           int* flags) {
+    const uint64_t t0 = global_ns();
+    for (uint32_t q = 0; q < n; ++q)
+        while ((int32_t)(ld_acquire_sys_u32(w + q) - e) < 0) {
+            if (global_ns() - t0 > timeout_ns) {
+                raise_flag(flags, 4);
+                return;
+            }
+            __nanosleep(64);
+        }
+}
+
+// Phase at kernel start (after grid_dep_wait: the kernels before this one on the stream
+// have completed and their stores are visible on this GPU).  CTA 0 makes them visible
+// system-wide (fence.sc.sys, cumulative over what this thread observed) and releases the
+// epoch into every peer's word; every CTA then acquires all of this rank's words.
+__device__ __forceinline__ void peer_pre(const ShardArgs& a) {
+    if (a.npre == 0) return;
     if (threadIdx.x == 0) {
         const uint32_t e = *reinterpret_cast<volatile const uint32_t*>(a.epoch);
-        const uint64_t t0 = global_ns();
-        bool late = false;
-        for (uint32_t q = 0; q < a.nwait && !late; ++q)
-            while ((int32_t)(ld_acquire_sys_u32(a.wait_at + q) - e) < 0) {
-                if (global_ns() - t0 > a.timeout_ns) {
-                    raise_flag(a.flags, 4);
-                    late = true;
-                    break;
-                }
-                __nanosleep(100);
-            }
+        if (blockIdx.x == 0) {
+            __threadfence_system();
+#pragma unroll
+            for (uint32_t q = 0; q < kMaxPeers; ++q)  // static indices: the parameter array stays in the constant bank
+                if (q < a.npre) st_release_sys_u32(a.pre_sig[q], e);
+        }
+        wait_words(a.pre_wait, a.npre, e, a.timeout_ns, a.flags);
     }
     __syncthreads();
 }
 
-// Peer phase signal (every thread of every CTA, after its last store): the CTA's stores
-// (peer memory over NVLink included) are made visible system-wide by thread 0's fence
-// after the barrier, then counted; the CTA that completes the count fences again, opens
-// the next epoch if asked, and releases the epoch into every peer's signal word.  One
-// system fence per CTA (the persistent grids have a few hundred), not per thread.
-__device__ __forceinline__ void peer_signal(const ShardArgs& a) {
-    if (a.nsig == 0) return;
+// Phase at kernel end (every thread of every CTA, after its last store).  The barrier
+// orders the CTA's stores (peer memory over NVLink included) before thread 0's release at
+// GPU scope (atom.release.gpu on the ticket); the CTA that completes the count has acquired
+// every CTA's release, so its fence.sc.sys is cumulative over the whole grid's stores and
+// its st.release.sys of the new epoch publishes them (PTX causality order is transitive
+// across the GPU- and system-scope links).  That CTA then waits for every peer's word of
+// the phase: the kernel completes only when every rank's stores of this phase have landed.
+// One system fence and one waiting CTA per launch.
+__device__ __forceinline__ void peer_post(const ShardArgs& a) {
+    if (a.npost == 0) return;
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
-        if (atomicAdd(a.ticket, 1u) == gridDim.x * gridDim.y - 1) {
+        uint32_t t;
+        asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(a.ticket) : "memory");
+        if (t == gridDim.x * gridDim.y - 1) {
             *reinterpret_cast<volatile uint32_t*>(a.ticket) = 0;  // the next launch counts from zero
             __threadfence_system();
-            uint32_t e = *reinterpret_cast<volatile uint32_t*>(a.epoch);
-            if (a.bump) *reinterpret_cast<volatile uint32_t*>(a.epoch) = ++e;
+            const uint32_t e = *reinterpret_cast<volatile uint32_t*>(a.epoch) + 1;
+            *reinterpret_cast<volatile uint32_t*>(a.epoch) = e;
 #pragma unroll
-            for (uint32_t q = 0; q < kMaxPeers; ++q)  // static indices: the parameter array stays in the constant bank
-                if (q < a.nsig) st_release_sys_u32(a.sig[q], e);
+            for (uint32_t q = 0; q < kMaxPeers; ++q)
+                if (q < a.npost) st_release_sys_u32(a.post_sig[q], e);
+            wait_words(a.post_wait, a.npost, e, a.timeout_ns, a.flags);
         }
     }
 }

@@ -51,6 +51,15 @@ constexpr int kWarps = 4;    // warps per CTA (persistent grid)
 #endif
 constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capped at 128)
 
+#ifndef TACO_XK_WARP_MAJOR
+#define TACO_XK_WARP_MAJOR 0
+#endif
+// first tile of a persistent warp (then every gridDim.x * kWarps-th): CTA-major gives the
+// trailing partial round to the first CTAs, warp-major spreads it over every CTA (and SM)
+__device__ __forceinline__ uint32_t first_tile(int warp) {
+    return TACO_XK_WARP_MAJOR ? (uint32_t)warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + (uint32_t)warp;
+}
+
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
 __host__ __device__ constexpr int bit(int v, int b) { return (v >> b) & 1; }
 
@@ -443,7 +452,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kWarps;
     const int qoff = q * 8;  // lane's element offset inside a vector row (chunk_off(0, q))
-    uint32_t t = blockIdx.x * kWarps + warp;
+    uint32_t t = first_tile(warp);
 
     // tile tt -> shard p, first block kk0 of the chunk, whether every block is whole
     struct Tile {
@@ -469,7 +478,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     };
 
     grid_dep_wait();
-    if constexpr (PUSH) peer_wait(a);  // fused peer mode: the peers have finished reading the slots this K1 writes
+    if constexpr (PUSH) peer_pre(a);  // fused peer mode: the peers have finished reading the slots this K1 writes
     Tile cur{0, 0, false};
     if (t < ntiles) {
         cur = info(t);
@@ -588,7 +597,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 #endif
         cur = nxt;
     }
-    if constexpr (PUSH) peer_signal(a);
+    if constexpr (PUSH) peer_post(a);  // ... and every rank's pushes of this phase have landed
 }
 
 // --------------------------------------------------------------------- K2 --------
@@ -674,8 +683,8 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     };
 
     grid_dep_wait();
-    peer_wait(a);  // fused peer mode: every rank's message has landed in the gather slots
-    uint32_t t = blockIdx.x * kWarps + warp;
+    peer_pre(a);  // fused peer mode: every rank's K3 has finished (its messages are in the gather slots)
+    uint32_t t = first_tile(warp);
 #pragma unroll
     for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
     int cur = 0;
@@ -706,7 +715,6 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
         store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, a.vec_ok, w);
     }
-    peer_signal(a);
 }
 
 // --------------------------------------------------------------------- K3 --------
@@ -726,7 +734,8 @@ constexpr int kMinCtasK3 = 3;
 
 template <int L, typename TAcc>
 __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg,
-                                         TAcc* __restrict__ acc_out, const ShardArgs& a, const CodecConsts& c) {
+                                         TAcc* __restrict__ acc_out, const ShardArgs& a, const CodecConsts& c,
+                                         uint64_t cta) {
     using K = K3X<L>;
     using D = DecPlan<L>;
     using Plan = typename D::Enc;
@@ -735,7 +744,7 @@ __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8
     const int lane = threadIdx.x & 31, q = lane & (L - 1), g = lane / L, warp = threadIdx.x >> 5;
     uint4* stage_base = smem_dyn + (size_t)warp * K::WARP_U4;
     uint4* code_buf = stage_base + NS * K::STAGE_U4;
-    const uint64_t kk0 = ((uint64_t)blockIdx.x * kWarps + warp) * G;
+    const uint64_t kk0 = (cta * kWarps + warp) * G;
     if (kk0 >= a.nblk) return;  // warp-uniform
     const uint64_t kk = kk0 + g;
     const bool live = kk < a.nblk;
@@ -844,16 +853,12 @@ __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8
     if (live && q == 0 && !ok) raise_flag(a.flags, 2);
 }
 
-// SYNC: the fused peer-signalling variant (taco_peer_*_dev); kept a separate instantiation
-// because the CTA-wide wait / signal costs the plain K3 ~40 bytes of register spills
-template <int L, typename TAcc, bool SYNC>
+template <int L, typename TAcc>
 __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     k3x(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg, TAcc* __restrict__ acc_out, ShardArgs a,
         CodecConsts c) {
     grid_dep_wait();
-    if constexpr (SYNC) peer_wait(a);  // every rank's copy of this shard has landed
-    k3x_warp<L, TAcc>(msgs, out_msg, acc_out, a, c);
-    if constexpr (SYNC) peer_signal(a);  // ... and the re-encoded shard is in every rank's gather slot
+    k3x_warp<L, TAcc>(msgs, out_msg, acc_out, a, c, blockIdx.x);
 }
 
 }  // namespace xk

@@ -16,17 +16,18 @@ s.close()
 dist.init_process_group("gloo")
 n = 8192 * 2560
 x = (torch.randn(n, device="cuda") * 1e-3).to(torch.bfloat16)
-par = peer.PeerTwoShotAllReduce(n, make_config(256), dtype=torch.bfloat16, device="cuda:0")
-out = torch.empty_like(x)
-for _ in range(int(os.environ.get("ITERS", "6"))):
-    par(x, out)
-torch.cuda.synchronize()
-par.check()
-start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-start.record()
-for _ in range(50):
-    par(x, out)
-end.record()
-torch.cuda.synchronize()
-print("peer step ms", start.elapsed_time(end) / 50)
-par.close()
+for fused in (True, False):
+    par = peer.PeerTwoShotAllReduce(n, make_config(256), dtype=torch.bfloat16, device="cuda:0", fused=fused)
+    out = torch.empty_like(x)
+    for _ in range(int(os.environ.get("ITERS", "6"))):
+        par(x, out)
+    torch.cuda.synchronize()
+    par.check()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record()
+    for _ in range(int(os.environ.get("REPS", "50"))):
+        par(x, out)
+    end.record()
+    torch.cuda.synchronize()
+    print(f"peer step ms fused={fused}", start.elapsed_time(end) / int(os.environ.get("REPS", "50")), flush=True)
+    par.close()
