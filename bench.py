@@ -574,7 +574,7 @@ def main():
     ap.add_argument("--block-sweep", type=lambda t: [int(v) for v in t.split(",")], default=[32, 64, 128, 256, 512],
                     help="N>1 configs[2]: Hadamard block sizes of the sequence-parallel sweep")
     ap.add_argument("--size-sweep", type=lambda t: [float(v) for v in t.split(",")] if t else [], default=None,
-                    help="N>1: configs[4] message sizes in MB (default 1,16,256 at N>1; empty string disables)")
+                    help="N>1: configs[4] message sizes in MB (default 1,16,256,1024 at N>1; empty string disables)")
     ap.add_argument("--collective", action="store_true", help="run the collective leg even at world size 1")
     ap.add_argument("--plan", action="store_true",
                     help="N>1: print what this N measures (workload, legs, NCCL comparators) without a GPU")
@@ -586,7 +586,7 @@ def main():
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.size_sweep is None:
-        args.size_sweep = [1.0, 16.0, 256.0] if (world > 1 or args.collective) else []
+        args.size_sweep = [1.0, 16.0, 256.0, 1024.0] if world > 1 else ([1.0, 16.0, 256.0] if args.collective else [])
     rank = int(os.environ.get("RANK", "0"))
     n_ranks = max(world, args.gpus) if args.impl == "reference" else world
     if args.shape:

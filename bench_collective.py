@@ -405,8 +405,11 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
             so = [torch.empty_like(v) for v in sx]
             sargs = type(args)(**{**vars(args), "steps": max(5, min(args.steps, 20)), "warmup": 3})
             _, _, _, _, r = _ar_leg(sargs, m_el, cfg, sx, so, stream, args.chunks)
+            c = 1 + 8 / args.block_size
+            hbm_bytes = m_el * (4 + 2 * c) + (world + 1) * c * m_el / world  # K1 + K2 + K3 per rank
             sw[f"{mb}MB"] = {"taco_ms": r["ms_per_step"], "nccl_bf16_ms": r["nccl_bf16_ms_per_step"],
-                             "speedup": r["speedup_vs_nccl_bf16"], "wire_frac_of_nvlink_900": r["wire_frac_of_nvlink_900"]}
+                             "speedup": r["speedup_vs_nccl_bf16"], "wire_frac_of_nvlink_900": r["wire_frac_of_nvlink_900"],
+                             "codec_hbm_frac": round(hbm_bytes / (r["ms_per_step"] * 1e-3) / (peaks()["hbm_gbs"] * 1e9), 4)}
             del sx, so
         extra["message_size_sweep"] = sw
 

@@ -56,8 +56,14 @@ constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capp
 #endif
 // first tile of a persistent warp (then every gridDim.x * kWarps-th): CTA-major gives the
 // trailing partial round to the first CTAs, warp-major spreads it over every CTA (and SM)
+// (measured, configs[1] / configs[3] tensors: warp-major K2 13.9 / 47.3 us vs 14.3 / 47.6;
+// K1 15.7 / 51.4 vs 15.6 / 51.2 -- K1 stays CTA-major)
+#ifndef TACO_XK_K2_WARP_MAJOR
+#define TACO_XK_K2_WARP_MAJOR 1
+#endif
+template <bool WARP_MAJOR = (TACO_XK_WARP_MAJOR != 0)>
 __device__ __forceinline__ uint32_t first_tile(int warp) {
-    return TACO_XK_WARP_MAJOR ? (uint32_t)warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + (uint32_t)warp;
+    return WARP_MAJOR ? (uint32_t)warp * gridDim.x + blockIdx.x : blockIdx.x * kWarps + (uint32_t)warp;
 }
 
 __host__ __device__ constexpr int ilog2c(int v) { return v <= 1 ? 0 : 1 + ilog2c(v >> 1); }
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 
     grid_dep_wait();
     peer_pre(a);  // fused peer mode: every rank's K3 has finished (its messages are in the gather slots)
-    uint32_t t = first_tile(warp);
+    uint32_t t = first_tile<TACO_XK_WARP_MAJOR || TACO_XK_K2_WARP_MAJOR>(warp);
 #pragma unroll
     for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
     int cur = 0;
