@@ -51,6 +51,9 @@ constexpr int kWarps = 4;    // warps per CTA (persistent grid)
 #endif
 constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capped at 128)
 
+#ifndef TACO_XK_SUMSQ_BF16
+#define TACO_XK_SUMSQ_BF16 1  // K1 bf16: sum of squares by fma.rn.f32.bf16 on the inputs (51.35 -> 50.75 us, configs[3])
+#endif
 #ifndef TACO_XK_WARP_MAJOR
 #define TACO_XK_WARP_MAJOR 0
 #endif
@@ -301,8 +304,10 @@ __device__ __forceinline__ bool sf_ok(float sf) { return sf < 0x1p100f && !(sf >
 // K1 does).  On return w holds the FP8-ready Z/s with canonical signs and zeros.
 template <int L, typename Plan, typename Reload>
 __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts& c, float& alpha, float& s,
-                                       double& ss, Reload reload) {
-    const float sf = sumsq_b0<Plan>(w);
+                                       double& ss, Reload reload, float sf_pre = -1.0f) {
+    // sf_pre >= 0: the lane's fp32 sum of squares was taken from the bf16 inputs (mixed-precision
+    // FMAs off the packed-FP32 pipe); otherwise from the b0-stage outputs
+    const float sf = sf_pre >= 0.0f ? sf_pre : sumsq_b0<Plan>(w);
     const bool lane_slow = !sf_ok(sf);
     float p2 = 1.0f;
     double sl = (double)sf;
@@ -530,7 +535,11 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         };
         float2 w[32];
         if (full) cp_wait<1>();  // this lane's chunks of tile t have landed
+        float sf_pre = -1.0f;
         if (sizeof(TIn) == 2 && full) {
+#if TACO_XK_SUMSQ_BF16
+            float sq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#endif
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
                 const uint4 u = sb[ch * 32];
@@ -538,15 +547,37 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
                 w[4 * ch + 1] = bf16_b0(u.y);
                 w[4 * ch + 2] = bf16_b0(u.z);
                 w[4 * ch + 3] = bf16_b0(u.w);
+#if TACO_XK_SUMSQ_BF16
+                const uint32_t uu[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    sq[k] = fma_bf16_sq(uu[k] & 0xffffu, sq[k]);
+                    sq[k] = fma_bf16_sq(uu[k] >> 16, sq[k]);
+                }
+#endif
             }
+#if TACO_XK_SUMSQ_BF16
+            sf_pre = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+#endif
         } else {
             load_plain(w);
+#if TACO_XK_SUMSQ_BF16
+            if (sizeof(TIn) == 2) {  // the full path's sum, same operations in the same order
+                float sq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    sq[i & 3] = __fmaf_rn(w[i].x, w[i].x, sq[i & 3]);
+                    sq[i & 3] = __fmaf_rn(w[i].y, w[i].y, sq[i & 3]);
+                }
+                sf_pre = (sq[0] + sq[1]) + (sq[2] + sq[3]);
+            }
+#endif
 #pragma unroll
             for (int i = 0; i < 32; ++i) w[i] = b0_f32(w[i]);
         }
         float alpha, s;
         double ss;
-        encode<L, Plan>(w, q, c, alpha, s, ss, load_plain);
+        encode<L, Plan>(w, q, c, alpha, s, ss, load_plain, sf_pre);
 #if TACO_XK_CSTORE
         {
             uint4 cv[4];
