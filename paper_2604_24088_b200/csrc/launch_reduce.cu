@@ -4,6 +4,9 @@
 #include "taco_tile.cuh"
 #include "taco_xk.cuh"
 
+#ifndef TACO_XK_K3_P2
+#define TACO_XK_K3_P2 1  // TP = 2 specialisation of K3 (both decodes in one straight-line block)
+#endif
 namespace taco_impl {
 using namespace taco_dev;
 
@@ -11,7 +14,7 @@ namespace {
 template <int L, typename T>
 cudaError_t run_xk(const Launch& l, const ShardArgs& a, const CodecConsts& c) {
     using K = xk::K3X<L>;
-    auto* kern = &xk::k3x<L, T>;
+    auto* kern = (a.P == 2 && TACO_XK_K3_P2) ? &xk::k3x<L, T, true> : &xk::k3x<L, T, false>;
     const uint64_t tiles = (a.nblk + K::G - 1) / K::G;
     const unsigned grid = (unsigned)((tiles + xk::kWarps - 1) / xk::kWarps);
     return launch_k(kern, grid, xk::kWarps * 32, K::SMEM, l.stream, static_cast<const uint8_t*>(l.in),

@@ -769,7 +769,7 @@ struct K3X {
 // K3 holds the running sum and one decoded rank at once (2 x 64 values): 3 CTAs per SM
 constexpr int kMinCtasK3 = 3;
 
-template <int L, typename TAcc>
+template <int L, typename TAcc, bool P2>
 __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg,
                                          TAcc* __restrict__ acc_out, const ShardArgs& a, const CodecConsts& c,
                                          uint64_t cta) {
@@ -796,7 +796,30 @@ __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8
     float2 acc[32];
     bool ok = true;
     int cur = 0;
-    for (uint32_t r = 0; r < a.P; ++r) {
+    if constexpr (P2) {
+        // two ranks (TP = 2): both tiles are staged by the prologue; the two decodes are one
+        // straight-line block the scheduler interleaves (no wait / barrier between them)
+        cp_wait<0>();
+        __syncwarp();
+        uint4 u0[4], u1[4];
+        float2 sc0 = make_float2(1.0f, 1.0f), sc1 = make_float2(1.0f, 1.0f);
+        if (live) {
+            read_lane_codes<L>(stage_base, g, q, u0);
+            sc0 = reinterpret_cast<const float2*>(stage_base + 128)[g];
+            read_lane_codes<L>(stage_base + K::STAGE_U4, g, q, u1);
+            sc1 = reinterpret_cast<const float2*>(stage_base + K::STAGE_U4 + 128)[g];
+        } else {
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch) u0[ch] = u1[ch] = make_uint4(0, 0, 0, 0);
+        }
+        ok = scalars_ok(sc0.x, sc0.y) && scalars_ok(sc1.x, sc1.y);
+        float2 y[32];
+        decode_block<L>(u0, sc0, live, q, c, acc);  // acc = decompress(rank 0) (collective.cpp:96)
+        decode_block<L>(u1, sc1, live, q, c, y);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) acc[i] = __fadd2_rn(acc[i], y[i]);  // acc[i] += part[i] (:99)
+    }
+    for (uint32_t r = 0; !P2 && r < a.P; ++r) {
         __syncwarp();  // every lane is done with the stage about to be refilled
         issue(r + NS - 1, cur == 0 ? NS - 1 : cur - 1);
         cp_wait<NS - 1>();
@@ -890,12 +913,12 @@ __device__ __forceinline__ void k3x_warp(const uint8_t* __restrict__ msgs, uint8
     if (live && q == 0 && !ok) raise_flag(a.flags, 2);
 }
 
-template <int L, typename TAcc>
+template <int L, typename TAcc, bool P2>
 __global__ void __launch_bounds__(kWarps * 32, kMinCtasK3)
     k3x(const uint8_t* __restrict__ msgs, uint8_t* __restrict__ out_msg, TAcc* __restrict__ acc_out, ShardArgs a,
         CodecConsts c) {
     grid_dep_wait();
-    k3x_warp<L, TAcc>(msgs, out_msg, acc_out, a, c, blockIdx.x);
+    k3x_warp<L, TAcc, P2>(msgs, out_msg, acc_out, a, c, blockIdx.x);
 }
 
 }  // namespace xk
