@@ -136,6 +136,63 @@ def test_peer_abi_argument_checks_without_a_gpu():
     assert lib.taco_last_error().decode() == "peer barrier timed out"
 
 
+def test_fused_peer_abi_checks_without_a_gpu():
+    """The fused (kernel-signalled) peer collectives validate the peer set, the config they
+    serve and the sync-word alignment before touching the device."""
+    import ctypes as C
+    lib = _abi.lib()
+    assert lib.taco_peer_flags_bytes() >= 4 * 35  # epoch, two phases of 8 words, tickets
+    assert lib.taco_peer_fused_supported(C.byref(make_config(256))) == 1
+    for b, fmt in ((32, 0), (1024, 0), (256, 1)):
+        assert lib.taco_peer_fused_supported(C.byref(make_config(b, fmt))) == 0
+    ps = _abi.Peers(); ps.nranks = 9
+    assert lib.taco_peer_allreduce_dev(C.byref(make_config()), None, 1, 100, C.byref(ps), 0, 0, 0, 0, None, 1, 10,
+                                       None, None) == _abi.ERR_USAGE
+    assert "1 to 8 ranks" in lib.taco_last_error().decode()
+    ps = _abi.Peers(); ps.nranks, ps.rank = 1, 0; ps.base[0] = 4096
+    for cfg in (make_config(256, 1), make_config(32)):
+        for rc in (lib.taco_peer_allreduce_dev(C.byref(cfg), None, 1, 100, C.byref(ps), 0, 0, 0, 0, None, 1, 10,
+                                               None, None),
+                   lib.taco_peer_reduce_scatter_dev(C.byref(cfg), None, 1, 100, C.byref(ps), 0, 0, 0, None, 1, 10,
+                                                    None, None),
+                   lib.taco_peer_all_gather_dev(C.byref(cfg), None, 1, 100, C.byref(ps), 0, 0, 0, None, 1, 10,
+                                                None, None)):
+            assert rc == _abi.ERR_USAGE and "fused peer signalling" in lib.taco_last_error().decode()
+    assert lib.taco_peer_allreduce_dev(C.byref(make_config()), None, 1, 100, C.byref(ps), 0, 0, 0, 8, None, 1, 10,
+                                       None, None) == _abi.ERR_USAGE
+    assert "16-byte aligned" in lib.taco_last_error().decode()
+    assert lib.taco_peer_allreduce_dev(C.byref(make_config()), None, 1, 0, C.byref(ps), 0, 0, 0, 0, None, 1, 10,
+                                       None, None) == _abi.ERR_INPUT
+    assert lib.taco_peer_check_access(0, 0) == _abi.OK
+
+
+def test_schedule_host_argument_checks_without_a_gpu():
+    """taco_allreduce_schedule_host (ring / tree / two-shot on the device) rejects what the
+    reference rejects (collective.cpp:24-33) before any device work."""
+    import ctypes as C
+    lib = _abi.lib()
+    cfg = make_config()
+    x = (C.c_float * 8)()
+    cases = ((None, 0, 2, 4, "null taco context", _abi.ERR_USAGE),)
+    for ctx, alg, p, n, msg, code in cases:
+        rc = lib.taco_allreduce_schedule_host(ctx, C.byref(cfg), alg, x, p, n, x, x, None)
+        assert rc == code and msg in lib.taco_last_error().decode()
+
+
+def test_chunked_nccl_workspace_sizes():
+    """Chunking never needs less workspace than one chunk (each chunk's messages are padded to
+    16 bytes); 0 chunks = the default (2); > 16 is refused (workspace 0)."""
+    import ctypes as C
+    lib = _abi.lib()
+    cfg = make_config()
+    n = 8192 * 2560
+    w = [lib.taco_collective_nccl_workspace_chunked(C.byref(cfg), 4, n, c) for c in (1, 2, 3, 16)]
+    assert w[0] > 0 and all(v >= w[0] for v in w)
+    assert lib.taco_collective_nccl_workspace(C.byref(cfg), 4, n) == w[1]
+    assert lib.taco_collective_nccl_workspace_chunked(C.byref(cfg), 4, n, 0) == w[1]
+    assert lib.taco_collective_nccl_workspace_chunked(C.byref(cfg), 4, n, 17) == 0
+
+
 @pytest.mark.parametrize("kind,n,seed", [(0, 100_003, 7), (1, 100_003, 7), (1, 262_144, 101), (1, 1, 3)])
 def test_generate_matches_reference(kind, n, seed, ref):
     # taco::generate (analysis.cpp:70-95) value for value: the bench's inputs are the
