@@ -323,7 +323,7 @@ __device__ __forceinline__ void encode(float2 (&w)[32], int q, const CodecConsts
     // the scalar chain sits in the same basic block as the butterfly, which does not depend
     // on it (alpha enters only through k), so the scheduler overlaps its latency
     ss = group_sum<L>(sl);
-    alpha = block_alpha_fast(ss, c);
+    alpha = block_alpha_xk(ss, c);
     Plan::stages(w, q);
     const float ymax = absmax32<L>(w);
     double k;
@@ -592,10 +592,14 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
             for (int c4 = 0; c4 < 4; ++c4) ov[c4] = code_buf[swz_unit(32 * c4 + lane)];
             const uint64_t kk0 = cur.kk0;
             auto put = [&](uint8_t* m) {
+                uint8_t* base = m + kk0 * B + 16 * lane;  // unit u = 32 c4 + lane at base + 512 c4
+                if (full) {
 #pragma unroll
-                for (int c4 = 0; c4 < 4; ++c4) {
-                    const int u = 32 * c4 + lane;
-                    if (full || kk0 + (uint64_t)((16 * u) / B) < a.nblk) st16_na(m + kk0 * B + 16 * (uint64_t)u, ov[c4]);
+                    for (int c4 = 0; c4 < 4; ++c4) st16_na(base + 512 * c4, ov[c4]);
+                } else {
+#pragma unroll
+                    for (int c4 = 0; c4 < 4; ++c4)
+                        if (kk0 + (uint64_t)((16 * (32 * c4 + lane)) / B) < a.nblk) st16_na(base + 512 * c4, ov[c4]);
                 }
                 if (q == 0 && (full || kk < a.nblk))
                     *reinterpret_cast<float2*>(m + a.scal_off + kk * 8) = make_float2(alpha, s);
