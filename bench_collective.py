@@ -140,6 +140,42 @@ def _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R):
             "barrier_kernels_per_step": 0 if par.fused else 2}
 
 
+def _abi_leg(args, n, cfg, xs, outs, step_ms, stream, R):
+    """The same two-shot through the C ABI on torch's own NCCL communicator
+    (taco_allreduce_nccl_chunked: one library call per step), CUDA-graph captured like the
+    Python-orchestrated leg and checked bit for bit against it on every rank."""
+    from paper_2604_24088_b200 import collective
+    from paper_2604_24088_b200._abi import TacoError
+
+    world = dist.get_world_size()
+    try:
+        car = collective.AbiTwoShotAllReduce(n, cfg, dtype=torch.bfloat16, chunks=args.chunks, device=xs[0].device)
+    except (TacoError, AttributeError, RuntimeError) as e:
+        return {"error": f"{type(e).__name__}: {e}"}
+    couts = [torch.empty_like(o) for o in outs]
+    graphs = [collective.Graphed(car, xs[i], couts[i]) for i in range(R)] if not args.eager else None
+
+    def cstep(i):
+        if graphs is not None:
+            graphs[i % R]()
+        else:
+            car(xs[i % R], couts[i % R])
+
+    for i in range(args.warmup):
+        cstep(i)
+    torch.cuda.synchronize()
+    ms = _timed(cstep, args.steps, stream) / args.steps
+    car(xs[0], couts[0])
+    torch.cuda.synchronize()
+    car.check()
+    same = torch.tensor([int(torch.equal(couts[0].view(torch.int16), outs[0].view(torch.int16)))], device=xs[0].device)
+    dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    return {"ms_per_step": round(ms, 5), "algbw_GBps": round(world * 2 * n / (ms * 1e-3) / 1e9, 1),
+            "speedup_vs_python_twoshot": round(step_ms / ms, 3),
+            "bit_identical_to_python_twoshot": bool(int(same.item()) == 1), "chunks": args.chunks,
+            "api": "taco_allreduce_nccl_chunked on ProcessGroupNCCL._comm_ptr()"}
+
+
 def _sp_leg(args, n, cfg, xs, stream, use_graphs, peer_leg=True):
     """CompressedReduceScatter of the [n] tensor and CompressedAllGather of its [n/P] slice,
     timed like the all-reduce, next to dist.reduce_scatter_tensor / all_gather_into_tensor
@@ -317,7 +353,8 @@ def plan(args, world: int) -> dict:
     """What `bench.py --gpus N` measures at this N, without touching a GPU (`--plan`): the
     workload, every leg and both bf16 NCCL comparators."""
     idx = args.config
-    legs = ["fp8_twoshot_allreduce (NCCL transport, chunked, CUDA graph)", "peer_memory_twoshot (fused signalling)"]
+    legs = ["fp8_twoshot_allreduce (NCCL transport, chunked, CUDA graph)", "peer_memory_twoshot (fused signalling)",
+            "c_abi_twoshot (taco_allreduce_nccl_chunked on torch's communicator)"]
     if idx == 2 or args.collective:
         legs += ["sequence_parallel reduce-scatter + all-gather (NCCL and peer transports)",
                  "sequence_parallel_block_sweep B in " + ",".join(str(b) for b in args.block_sweep)]
@@ -372,6 +409,9 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
     # the same all-reduce with the exchange done by the kernels' own stores into the peers'
     # memory (peer.py): no NCCL call on the data path; must be bit-identical to the above
     peer_rep = _peer_leg(args, n, cfg, xs, outs, ar, step_ms, stream, R)
+    # outs[0] holds the Python two-shot's result of xs[0] (the peer leg's last check)
+    ar(xs[0], outs[0])
+    abi_rep = _abi_leg(args, n, cfg, xs, outs, step_ms, stream, R)
 
     extra = {}
     if idx == 2 or args.collective:
@@ -473,6 +513,7 @@ def run_collective(args, rows, cols, clock_sampler, peaks):
                     "ms_per_step": round(e2e_ms, 4), "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 2 * n,
                     "api": "collective.TwoShotAllReduce (pinned host in / out)"},
             "peer_memory_twoshot": peer_rep,
+            "c_abi_twoshot": abi_rep,
             **extra,
             "ranks_agree": bool(abs(float(mx.item()) - float(mn.item())) == 0.0),
             "gpu_launches": 3 * len(ar.ch.ranges) * args.steps,

@@ -23,6 +23,8 @@ same message format so the schedule itself is exercised under gloo.
 """
 from __future__ import annotations
 
+import ctypes as _ct
+
 import torch
 import torch.distributed as dist
 
@@ -227,3 +229,112 @@ class Graphed:
     def __call__(self):
         self.graph.replay()
         return self.out
+
+
+def nccl_comm_ptr(group=None, device=None) -> int:
+    """The ncclComm_t behind a torch.distributed NCCL group (ProcessGroupNCCL._comm_ptr), the
+    communicator is created first if torch has not used it yet."""
+    pg = group if group is not None else dist.group.WORLD
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    backend = pg._get_backend(dev)
+    ptr = int(backend._comm_ptr())
+    if ptr == 0:  # lazily initialised communicator: one tiny collective creates it
+        t = torch.zeros(1, device=dev)
+        dist.all_reduce(t, group=pg)
+        torch.cuda.synchronize(dev)
+        ptr = int(backend._comm_ptr())
+    if ptr == 0:
+        raise _abi.TacoError(_abi.ERR_USAGE, "the group has no NCCL communicator")
+    return ptr
+
+
+class _AbiCollective:
+    """Base of the C-ABI collectives on torch's own NCCL communicator: one library call per
+    collective issues every codec kernel on the caller's stream and every NCCL call on the
+    library's communication stream (include/taco_b200.h taco_*_nccl_chunked), so a step
+    costs one host call instead of a Python round trip per chunk and op."""
+
+    def __init__(self, n_total: int, cfg: Config | None, group, dtype, out_dtype, chunks: int, device):
+        self.group = group
+        self.P = dist.get_world_size(group)
+        self.cfg = cfg if cfg is not None else _abi.make_config()
+        self.dtype = dtype
+        self.out_dtype = out_dtype or dtype
+        self.chunks = chunks
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.comm = nccl_comm_ptr(group, self.device)
+        lib = _abi.lib()
+        ws = int(lib.taco_collective_nccl_workspace_chunked(_ct.byref(self.cfg), self.P, n_total, chunks))
+        if ws == 0:
+            raise _abi.TacoError(_abi.ERR_USAGE, "no workspace for this geometry (chunks must be 1 to 16)")
+        self.work = torch.empty(ws, dtype=torch.uint8, device=self.device)
+        self.flags = dev.Flags(self.device)
+
+    def _call(self, fn: str, x: torch.Tensor, n: int, out: torch.Tensor, stream=None):
+        st = _ct.c_void_p(stream.cuda_stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream)
+        _abi.check(getattr(_abi.lib(), fn)(_ct.byref(self.cfg), _ct.c_void_p(x.data_ptr()), dev._dtype_code(x.dtype), n,
+                                           _ct.c_void_p(out.data_ptr()), dev._dtype_code(out.dtype),
+                                           _ct.c_void_p(self.work.data_ptr()), _ct.c_void_p(self.comm),
+                                           self.flags.ptr(), st, self.chunks))
+        return out
+
+    def _check_in(self, x: torch.Tensor, n: int) -> torch.Tensor:
+        x = x.reshape(-1)
+        if x.device != self.device:
+            raise _abi.TacoError(_abi.ERR_USAGE, f"input must live on {self.device}")
+        if x.numel() != n:
+            raise _abi.TacoError(_abi.ERR_INPUT, "all rank inputs must have the same length")
+        return x.contiguous()
+
+    def _out(self, out, numel):
+        if out is None:
+            return torch.empty(numel, dtype=self.out_dtype, device=self.device)
+        if not out.is_contiguous() or out.numel() != numel or out.device != self.device:
+            raise _abi.TacoError(_abi.ERR_USAGE, f"out must be a contiguous tensor of {numel} elements on {self.device}")
+        return out
+
+    def check(self):
+        self.flags.check()
+
+
+class AbiTwoShotAllReduce(_AbiCollective):
+    """TwoShotAllReduce through taco_allreduce_nccl_chunked on the group's own communicator
+    (bit-identical to TwoShotAllReduce with the same chunking)."""
+
+    def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 chunks: int = 2, device=None):
+        super().__init__(n, cfg, group, dtype, out_dtype, chunks, device)
+        self.n = n
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        x = self._check_in(x, self.n)
+        return self._call("taco_allreduce_nccl_chunked", x, self.n, self._out(out, self.n), stream)
+
+
+class AbiReduceScatter(_AbiCollective):
+    """CompressedReduceScatter through taco_reduce_scatter_nccl_chunked: [n] -> [ceil(n/P)]."""
+
+    def __init__(self, n: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 chunks: int = 2, device=None):
+        super().__init__(n, cfg, group, dtype, out_dtype, chunks, device)
+        self.n = n
+        self.shard_len = cdiv(n, self.P)
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        x = self._check_in(x, self.n)
+        return self._call("taco_reduce_scatter_nccl_chunked", x, self.n, self._out(out, self.shard_len), stream)
+
+
+class AbiAllGather(_AbiCollective):
+    """CompressedAllGather through taco_all_gather_nccl_chunked: [n_local] -> [P * n_local]."""
+
+    def __init__(self, n_local: int, cfg: Config | None = None, group=None, dtype=torch.bfloat16, out_dtype=None,
+                 chunks: int = 2, device=None):
+        P = dist.get_world_size(group)
+        super().__init__(P * n_local, cfg, group, dtype, out_dtype, chunks, device)
+        self.n_local = n_local
+
+    def __call__(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        x = self._check_in(x, self.n_local)
+        return self._call("taco_all_gather_nccl_chunked", x, self.n_local, self._out(out, self.P * self.n_local),
+                          stream)

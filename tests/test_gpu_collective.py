@@ -196,3 +196,34 @@ def test_reduce_encode_pointer_array_matches_strided(port, b, P):
     torch.cuda.synchronize()
     assert torch.equal(got[: lay.msg_bytes], want[: lay.msg_bytes])
     assert torch.equal(acc_g.view(torch.int32), acc_w.view(torch.int32))
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 5])
+def test_abi_collectives_on_torch_communicator(port, nccl_world1, chunks):
+    """The C-ABI collectives on torch's own NCCL communicator (one library call per step)
+    equal the Python-orchestrated collectives bit for bit, eagerly and graph-replayed."""
+    n = 8192 * 40 + 3
+    cfg = make_config(256)
+    x = torch.from_numpy(port.mixture(n, 9)).cuda().to(torch.bfloat16)
+    ar = collective.AbiTwoShotAllReduce(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=chunks)
+    want = collective.TwoShotAllReduce(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=chunks)(x)
+    got = ar(x)
+    torch.cuda.synchronize()
+    ar.check()
+    assert torch.equal(got.view(torch.int32), want.view(torch.int32))
+    out = torch.full((n,), float("nan"), device="cuda")
+    g = collective.Graphed(ar, x, out)
+    out.fill_(float("nan"))
+    g()
+    torch.cuda.synchronize()
+    assert torch.equal(out.view(torch.int32), want.view(torch.int32))
+    rs = collective.AbiReduceScatter(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32, chunks=chunks)
+    want_rs = collective.CompressedReduceScatter(n, cfg, dtype=torch.bfloat16, out_dtype=torch.float32,
+                                                 chunks=chunks)(x)
+    assert torch.equal(rs(x).view(torch.int32), want_rs.view(torch.int32))
+    ag = collective.AbiAllGather(n, cfg, dtype=torch.bfloat16, out_dtype=torch.bfloat16, chunks=chunks)
+    want_ag = collective.CompressedAllGather(n, cfg, dtype=torch.bfloat16, out_dtype=torch.bfloat16, chunks=chunks)(x)
+    assert torch.equal(ag(x), want_ag)
+    torch.cuda.synchronize()
+    rs.check()
+    ag.check()
