@@ -74,9 +74,20 @@ class TpContext:
             cls = {"ar": peer.PeerTwoShotAllReduce, "rs": peer.PeerReduceScatter, "ag": peer.PeerAllGather}[kind]
             op = cls(n, self.cfg, self.group, dtype=dtype, device=device)
         else:
-            cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
-                   "ag": collective.CompressedAllGather}[kind]
-            op = cls(n, self.cfg, self.group, dtype=dtype, chunks=self.chunks, device=device, codec=self.codec)
+            op = None
+            if self.codec is None and device.type == "cuda" and dist.get_backend(self.group) == "nccl":
+                # the C-ABI schedule on the group's own communicator: one library call per
+                # collective instead of a Python call per chunk and op (same numerics)
+                abi_cls = {"ar": collective.AbiTwoShotAllReduce, "rs": collective.AbiReduceScatter,
+                           "ag": collective.AbiAllGather}[kind]
+                try:
+                    op = abi_cls(n, self.cfg, self.group, dtype=dtype, chunks=max(1, self.chunks), device=device)
+                except (AttributeError, RuntimeError, _abi.TacoError):
+                    op = None  # no communicator handle in this torch build: the Python schedule
+            if op is None:
+                cls = {"ar": collective.TwoShotAllReduce, "rs": collective.CompressedReduceScatter,
+                       "ag": collective.CompressedAllGather}[kind]
+                op = cls(n, self.cfg, self.group, dtype=dtype, chunks=self.chunks, device=device, codec=self.codec)
         self._ops[k] = op
         while len(self._ops) > _MAX_CACHED:
             _close(self._ops.popitem(last=False)[1])
