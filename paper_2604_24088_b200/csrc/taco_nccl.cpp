@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -29,6 +30,8 @@ struct Nccl {
     ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    // NCCL >= 2.28: the native all-to-all (optional; grouped send/recv otherwise)
+    ncclResult_t (*all_to_all)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*count)(const ncclComm_t, int*) = nullptr;
     ncclResult_t (*user_rank)(const ncclComm_t, int*) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
@@ -51,6 +54,8 @@ const Nccl& nccl() {
         n.send = reinterpret_cast<decltype(n.send)>(sym("ncclSend"));
         n.recv = reinterpret_cast<decltype(n.recv)>(sym("ncclRecv"));
         n.all_gather = reinterpret_cast<decltype(n.all_gather)>(sym("ncclAllGather"));
+        n.all_to_all = reinterpret_cast<decltype(n.all_to_all)>(sym("ncclAlltoAll"));
+        if (const char* v = std::getenv("TACO_NCCL_ALLTOALL"); v && std::strcmp(v, "0") == 0) n.all_to_all = nullptr;
         n.count = reinterpret_cast<decltype(n.count)>(sym("ncclCommCount"));
         n.user_rank = reinterpret_cast<decltype(n.user_rank)>(sym("ncclCommUserRank"));
         n.error_string = reinterpret_cast<decltype(n.error_string)>(sym("ncclGetErrorString"));
@@ -105,6 +110,8 @@ int all_to_all(const uint8_t* send, uint8_t* recv, uint64_t stride, uint64_t byt
     const Nccl& n = nccl();
     auto c = static_cast<ncclComm_t>(comm);
     auto st = static_cast<cudaStream_t>(stream);
+    if (n.all_to_all && bytes == stride)  // dense [P][stride] buffers: the native collective
+        return nccl_check(n.all_to_all(send, recv, bytes, ncclUint8, c, st));
     if (int rc = nccl_check(n.group_start())) return rc;
     for (int r = 0; r < g.P; ++r) {
         if (int rc = nccl_check(n.send(send + r * stride, bytes, ncclUint8, r, c, st))) return rc;
