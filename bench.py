@@ -280,6 +280,8 @@ class CollectiveCodecBench:
         self.send = [torch.empty(P * st, dtype=torch.uint8, device=dev) for _ in range(self.R)]
         self.red = [torch.empty(st, dtype=torch.uint8, device=dev) for _ in range(self.R)]
         self.ys = [torch.empty(self.n, dtype=torch.bfloat16, device=dev) for _ in range(self.R)]
+        self.sp = [torch.empty(self.S, dtype=torch.bfloat16, device=dev) for _ in range(self.R)]  # SP RS output
+        self.slice_msg = [torch.empty(st, dtype=torch.uint8, device=dev) for _ in range(self.R)]
         self.flags = codec.Flags(dev)
         self.lib = _abi.lib()
 
@@ -299,6 +301,18 @@ class CollectiveCodecBench:
             C.byref(self.cfg), C.c_void_p(self.send[i].data_ptr()), self.lay.msg_stride, self.P, self.S, 0, self.m,
             C.c_void_p(self.red[i].data_ptr()), None, 0, self.flags.ptr(), self._st()))
 
+    def k3rs(self, i):  # sequence-parallel reduce-scatter: the bf16 stage-1 sum is the product
+        import ctypes as C
+        self._abi.check(self.lib.taco_reduce_encode_dev(
+            C.byref(self.cfg), C.c_void_p(self.send[i].data_ptr()), self.lay.msg_stride, self.P, self.S, 0, self.m,
+            None, C.c_void_p(self.sp[i].data_ptr()), self._abi.DT_BF16, self.flags.ptr(), self._st()))
+
+    def k1slice(self, i):  # sequence-parallel all-gather: compress of the own [S] slice
+        import ctypes as C
+        self._abi.check(self.lib.taco_compress_dev(
+            C.byref(self.cfg), C.c_void_p(self.xs[i].data_ptr()), self._abi.DT_BF16, self.S, 1, 0, self.m,
+            C.c_void_p(self.slice_msg[i].data_ptr()), self.lay.msg_stride, self.flags.ptr(), self._st()))
+
     def k2(self, i):
         import ctypes as C
         self._abi.check(self.lib.taco_decompress_dev(
@@ -313,9 +327,11 @@ class CollectiveCodecBench:
                 self.k1(i)
                 self.k3(i)
                 self.k2(i)
+                self.k3rs(i)
+                self.k1slice(i)
             stream.synchronize()
             self.flags.check()
-            for name in ("k1", "k3", "k2"):
+            for name in ("k1", "k3", "k2", "k3rs", "k1slice"):
                 fn = getattr(self, name)
                 g = _graph(lambda: [fn((s + 1) % self.R) for s in range(steps)], stream)
                 g.replay()
@@ -352,6 +368,13 @@ def collective_budget(args, dev, stream, pk) -> dict:
             "k3_frac_of_hbm": round(k3_bytes / (t["k3"] * 1e-3) / 1e9 / pk["hbm_gbs"], 4),
             "fp8_wire_us_at_900GBps": round(wire_fp8 / (nvlink * 1e9) * 1e6, 2),
             "bf16_ring_wire_us_at_900GBps": round(wire_bf16 / (nvlink * 1e9) * 1e6, 2),
+            # sequence-parallel pair on the same tensor: RS = K1 (P shards) + K3 (bf16 sum, no
+            # re-encode); AG = K1 of the own [S] slice + K2 of the P gathered slices; each moves
+            # (P-1) messages per rank (bf16: (P-1)/P * 2n bytes)
+            "sp_reduce_scatter_codec_us": round((t["k1"] + t["k3rs"]) * 1e3, 2),
+            "sp_all_gather_codec_us": round((t["k1slice"] + t["k2"]) * 1e3, 2),
+            "sp_fp8_wire_us_each": round((P - 1) * st.msg_bytes / (nvlink * 1e9) * 1e6, 2),
+            "sp_bf16_wire_us_each": round((P - 1) * 2 * n / P / (nvlink * 1e9) * 1e6, 2),
         }
         del cb
     return res
