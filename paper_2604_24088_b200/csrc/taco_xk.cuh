@@ -51,6 +51,13 @@ constexpr int kWarps = 4;    // warps per CTA (persistent grid)
 #endif
 constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capped at 128)
 
+#ifndef TACO_XK_K1_F32_DIRECT
+// fp32-input K1 without shared-memory staging: 119.9 -> 72.2 us (0.54 -> 0.89 of HBM) on
+// configs[3]; the staged form saturated the MIO pipe (16 LDGSTS + 16 LDS.128 + 70 SHFL per
+// lane-tile, mio_throttle 2.4 and short_scoreboard 2.8 stalls per issue, issue active 0.28).
+// bf16 keeps the staging (direct loads: 55.7 vs 50.7 us).
+#define TACO_XK_K1_F32_DIRECT 1
+#endif
 #ifndef TACO_XK_SUMSQ_BF16
 #define TACO_XK_SUMSQ_BF16 1  // K1 bf16: sum of squares by fma.rn.f32.bf16 on the inputs (51.35 -> 50.75 us, configs[3])
 #endif
@@ -419,7 +426,11 @@ struct K1X {
     static constexpr int B = 64 * L, G = 32 / L;
     static constexpr int EPC = 16 / (int)sizeof(TIn);  // elements per 16-byte chunk
     static constexpr int NCH = 64 / EPC;              // chunks per lane per tile
-    static constexpr int STAGES = 2;
+    // fp32 input (TACO_XK_K1_F32_DIRECT): no shared-memory staging -- the lane's chunks are
+    // loaded straight into registers (the ragged path's vector loads), which leaves the MIO
+    // pipe to the exchanges; 16 warps per SM hide the load latency
+    static constexpr bool DIRECT = sizeof(TIn) == 4 && TACO_XK_K1_F32_DIRECT;
+    static constexpr int STAGES = DIRECT ? 0 : 2;
     static constexpr int STAGE_U4 = NCH * 32;
 #ifndef TACO_XK_CSTORE
 #define TACO_XK_CSTORE 1  // codes staged through shared memory: 54.0 -> 51.4 us (configs[3], bf16)
@@ -479,7 +490,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         return Tile{p, kk0, a.vec_ok && kk0 + G <= (p == plast ? flast : fmid)};
     };
     auto issue = [&](const Tile& tl, int stage) {
-        if (tl.full) {
+        if (tl.full && !K::DIRECT) {
             const TIn* src = x + (tl.p * a.S + (a.blk0 + tl.kk0 + g) * B) + qoff;
             uint4* sb = stage_base + stage * K::STAGE_U4;
 #pragma unroll
@@ -509,7 +520,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         const bool full = cur.full;
         // plain (pre-b0) values of the lane in the natural layout: pair 4j + r/2
         auto load_plain = [&](float2 (&w)[32]) {
-            if (full) {
+            if (full && !K::DIRECT) {
 #pragma unroll
                 for (int ch = 0; ch < NCH; ++ch) plain_from_chunk<TIn>(sb[ch * 32], &w[ch * (EPC / 2)]);
             } else {
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
             }
         };
         float2 w[32];
-        if (full) cp_wait<1>();  // this lane's chunks of tile t have landed
+        if (full && !K::DIRECT) cp_wait<1>();  // this lane's chunks of tile t have landed
         float sf_pre = -1.0f;
         if (sizeof(TIn) == 2 && full) {
 #if TACO_XK_SUMSQ_BF16
