@@ -108,6 +108,11 @@ taco_layout layout_of(uint64_t pb, uint64_t nblocks) {  // pb = payload bytes pe
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+// ShardArgs::vec_ok: 2 = 32-byte aligned (256-bit vector access), 1 = 16-byte aligned, 0 = scalar
+int vec_align(const void* p) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    return (a & 31u) == 0 ? 2 : (a & 15u) == 0 ? 1 : 0;
+}
 
 // Messages are read and written with 16-byte vector / TMA accesses: every message base must
 // be 16-byte aligned, i.e. the buffer and (with more than one message) the stride.
@@ -273,7 +278,7 @@ int taco_compress_dev(const taco_config* cfg, const void* x, int dtype, uint64_t
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if (int rc = check_msg_buffer(msgs, msg_stride, shards, "messages")) return rc;
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
-                aligned16(x) && (shards == 1 || S % 8 == 0), d_flags};
+                ((shards == 1 || S % 8 == 0) ? vec_align(x) : 0), d_flags};
     taco_dev::with_full_blocks(a, b);
     Launch l{cfg->block_size, dtype, (int)cfg->format, x, msgs, nullptr, (cudaStream_t)stream};
     if (cfg->kind != 0) {
@@ -300,7 +305,7 @@ int taco_decompress_dev(const taco_config* cfg, const void* msgs, uint64_t msg_s
     if (shards > 1 && msg_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if (int rc = check_msg_buffer(msgs, msg_stride, shards, "messages")) return rc;
     ShardArgs a{n, S, shards, blk_begin, blk_end - blk_begin, msg_stride, lay.scal_offset,
-                aligned16(out) && (shards == 1 || S % 8 == 0), d_flags};
+                ((shards == 1 || S % 8 == 0) ? vec_align(out) : 0), d_flags};
     taco_dev::with_full_blocks(a, b);
     Launch l{cfg->block_size, out_dtype, (int)cfg->format, msgs, out, nullptr, (cudaStream_t)stream};
     if (cfg->kind != 0) {
@@ -332,7 +337,7 @@ int taco_reduce_encode_dev(const taco_config* cfg, const void* msgs, uint64_t ra
     if (out_msg)
         if (int rc = check_msg_buffer(out_msg, 0, 1, "out_msg")) return rc;
     ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
-                acc_out ? aligned16(acc_out) : 0, d_flags};
+                acc_out ? vec_align(acc_out) : 0, d_flags};
     taco_dev::with_full_blocks(a, b);
     a.full_last = a.full_mid;  // every rank's message covers the same (single) shard
     Launch l{cfg->block_size, acc_dtype, (int)cfg->format, msgs, out_msg, acc_out, (cudaStream_t)stream};
@@ -446,7 +451,7 @@ int taco_compress_push_dev(const taco_config* cfg, const void* x, int dtype, uin
     if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
     ShardArgs a{n, S, P, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset,
-                aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+                ((P == 1 || S % 8 == 0) ? vec_align(x) : 0), d_flags};
     taco_dev::with_full_blocks(a, b);
     for (uint32_t q = 0; q < P; ++q)
         a.dst[q] = static_cast<uint8_t*>(peers->base[q]) + dst_offset + (uint64_t)peers->rank * slot_stride;
@@ -468,7 +473,7 @@ int taco_compress_bcast_dev(const taco_config* cfg, const void* x, int dtype, ui
     const taco_layout lay = layout_of(b, blk_end - blk_begin);
     if (peers->nranks > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
-    ShardArgs a{n, n, 1, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset, aligned16(x), d_flags};
+    ShardArgs a{n, n, 1, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset, vec_align(x), d_flags};
     taco_dev::with_full_blocks(a, b);
     for (uint32_t q = 0; q < peers->nranks; ++q)
         a.dst[q] = static_cast<uint8_t*>(peers->base[q]) + dst_offset + (uint64_t)peers->rank * slot_stride;
@@ -496,7 +501,7 @@ int taco_reduce_encode_push_dev(const taco_config* cfg, const void* msgs, uint64
     if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((dst_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
     ShardArgs a{shard_len, shard_len, P, blk_begin, blk_end - blk_begin, rank_stride, lay.scal_offset,
-                acc_out ? aligned16(acc_out) : 0, d_flags};
+                acc_out ? vec_align(acc_out) : 0, d_flags};
     taco_dev::with_full_blocks(a, b);
     a.full_last = a.full_mid;
     for (uint32_t q = 0; q < P; ++q)
@@ -576,7 +581,7 @@ int taco_peer_allreduce_dev(const taco_config* cfg, const void* x, int dtype, ui
     cudaStream_t st = (cudaStream_t)stream;
     // K1: push shard p into rank p's receive slot [me]; its last CTA opens the epoch,
     // publishes phase A and waits for every peer's (all P copies of my shard have landed)
-    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, ((P == 1 || S % 8 == 0) ? vec_align(x) : 0), d_flags};
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
     a1.ndst = P;
@@ -595,7 +600,7 @@ int taco_peer_allreduce_dev(const taco_config* cfg, const void* x, int dtype, ui
         return cuda_fail(e, "K3 reduce-encode launch");
     // K2: publish phase B (my K3 is done: my receive slots are free, my gather pushes are
     // out), wait for every peer's, decode locally
-    ShardArgs a2{n, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || S % 8 == 0), d_flags};
+    ShardArgs a2{n, S, P, 0, m, slot_stride, lay.scal_offset, ((P == 1 || S % 8 == 0) ? vec_align(out) : 0), d_flags};
     taco_dev::with_full_blocks(a2, b);
     set_pre(a2, peers, flags_offset, kPhaseB, timeout_ms);
     Launch l2{cfg->block_size, out_dtype, (int)cfg->format, own + gath_offset, out, nullptr, st};
@@ -617,7 +622,7 @@ int taco_peer_reduce_scatter_dev(const taco_config* cfg, const void* x, int dtyp
     if (P > 1 && slot_stride < lay.msg_bytes) return fail(TACO_ERR_USAGE, "message stride too small");
     if ((recv_offset | slot_stride) % 16) return fail(TACO_ERR_USAGE, "peer slots must be 16-byte aligned");
     cudaStream_t st = (cudaStream_t)stream;
-    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x) && (P == 1 || S % 8 == 0), d_flags};
+    ShardArgs a1{n, S, P, 0, m, lay.msg_stride, lay.scal_offset, ((P == 1 || S % 8 == 0) ? vec_align(x) : 0), d_flags};
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + recv_offset + me * slot_stride;
     a1.ndst = P;
@@ -628,7 +633,7 @@ int taco_peer_reduce_scatter_dev(const taco_config* cfg, const void* x, int dtyp
     Launch l1{cfg->block_size, dtype, (int)cfg->format, x, a1.dst[0], nullptr, st};
     if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
     // K3 (plain) with the fp32 (or bf16) stage-1 sum as the product
-    ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, aligned16(out), d_flags};
+    ShardArgs a3{S, S, P, 0, m, slot_stride, lay.scal_offset, vec_align(out), d_flags};
     taco_dev::with_full_blocks(a3, b);
     a3.full_last = a3.full_mid;
     const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
@@ -654,7 +659,7 @@ int taco_peer_all_gather_dev(const taco_config* cfg, const void* x, int dtype, u
     // K1 broadcast of the own slice into every rank's gather slot [me]: phase B first (every
     // peer's K2 of the previous call is done with the gather slots), then phase A (every
     // rank's broadcast has landed)
-    ShardArgs a1{n_local, n_local, 1, 0, m, lay.msg_stride, lay.scal_offset, aligned16(x), d_flags};
+    ShardArgs a1{n_local, n_local, 1, 0, m, lay.msg_stride, lay.scal_offset, vec_align(x), d_flags};
     taco_dev::with_full_blocks(a1, b);
     for (uint32_t q = 0; q < P; ++q) a1.dst[q] = static_cast<uint8_t*>(peers->base[q]) + gath_offset + me * slot_stride;
     a1.ndst = P;
@@ -665,7 +670,7 @@ int taco_peer_all_gather_dev(const taco_config* cfg, const void* x, int dtype, u
     if (cudaError_t e = taco_impl::launch_compress(l1, a1, consts_of(cfg))) return cuda_fail(e, "K1 compress launch");
     // K2 (plain) of the P gathered slices
     const uint64_t n = (uint64_t)P * n_local;
-    ShardArgs a2{n, n_local, P, 0, m, slot_stride, lay.scal_offset, aligned16(out) && (P == 1 || n_local % 8 == 0),
+    ShardArgs a2{n, n_local, P, 0, m, slot_stride, lay.scal_offset, ((P == 1 || n_local % 8 == 0) ? vec_align(out) : 0),
                  d_flags};
     taco_dev::with_full_blocks(a2, b);
     const uint8_t* own = static_cast<const uint8_t*>(peers->base[me]);
@@ -697,7 +702,7 @@ int taco_reduce_encode_ptrs_dev(const taco_config* cfg, const void* const* msgs,
     if (b > 1024) return fail(TACO_ERR_USAGE, "pointer-array reduction supports block sizes up to 1024");
     const taco_layout lay = layout_of(b, blk_end - blk_begin);
     ShardArgs a{shard_len, shard_len, nranks, blk_begin, blk_end - blk_begin, lay.msg_stride, lay.scal_offset,
-                acc_out ? aligned16(acc_out) : 0, d_flags};
+                acc_out ? vec_align(acc_out) : 0, d_flags};
     taco_dev::with_full_blocks(a, b);
     a.full_last = a.full_mid;
     for (uint32_t r = 0; r < nranks; ++r) a.src[r] = static_cast<const uint8_t*>(msgs[r]);

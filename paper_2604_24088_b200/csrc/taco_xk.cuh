@@ -364,11 +364,26 @@ __device__ __forceinline__ void st16_na(void* p, uint4 v) {
                  : "memory");
 }
 
-// 8 contiguous outputs (4 pairs) of type T
+// 256-bit global accesses (sm_100: LDG.256 / STG.256), 32-byte aligned addresses only
+__device__ __forceinline__ void ldg32_f32(const float* p, float2 (&o)[4]) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(o[0].x), "=f"(o[0].y), "=f"(o[1].x), "=f"(o[1].y), "=f"(o[2].x), "=f"(o[2].y), "=f"(o[3].x),
+                   "=f"(o[3].y)
+                 : "l"(p));
+}
+__device__ __forceinline__ void stg32_f32(float* p, const float2* v) {
+    asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0].x),
+                 "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y)
+                 : "memory");
+}
+
+// 8 contiguous outputs (4 pairs) of type T; wide: 32-byte aligned (one 256-bit store for fp32)
 template <typename T>
-__device__ __forceinline__ void store8(T* p, const float2* v) {
+__device__ __forceinline__ void store8(T* p, const float2* v, bool wide = false) {
     if constexpr (sizeof(T) == 2) {
         st16_na(p, make_uint4(pack_bf16x2(v[0]), pack_bf16x2(v[1]), pack_bf16x2(v[2]), pack_bf16x2(v[3])));
+    } else if (wide) {
+        stg32_f32(p, v);
     } else {
         st16_na(p, make_uint4(__float_as_uint(v[0].x), __float_as_uint(v[0].y), __float_as_uint(v[1].x),
                               __float_as_uint(v[1].y)));
@@ -388,12 +403,12 @@ __device__ __forceinline__ void store8_guarded(T* p, int pos, int valid, const f
 // K2/K3 decode output layout: lane q holds, for vector v (pairs 4v..4v+3), the 8 outputs at
 // block position lane_off(q) + vec_pos(v)
 template <int L, typename T>
-__device__ __forceinline__ void store_decoded(T* blk, int q, int valid, bool vec_ok, const float2 (&w)[32]) {
+__device__ __forceinline__ void store_decoded(T* blk, int q, int valid, int vec_ok, const float2 (&w)[32]) {
     using D = DecPlan<L>;
     const int lo = D::lane_off(q);
     if (vec_ok && valid == 64 * L) {
 #pragma unroll
-        for (int v = 0; v < 8; ++v) store8<T>(blk + lo + D::vec_pos(v), &w[4 * v]);
+        for (int v = 0; v < 8; ++v) store8<T>(blk + lo + D::vec_pos(v), &w[4 * v], vec_ok >= 2);
     } else {
 #pragma unroll
         for (int v = 0; v < 8; ++v) {
@@ -537,7 +552,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
                 for (int j = 0; j < 8; ++j) {
                     const int pos = (j * L + qq) * 8;
                     float2 tmp[4];
-                    if (a.vec_ok && pos + 8 <= valid) load_vec<TIn, 8>(src + pos, tmp);
+                    if (sizeof(TIn) == 4 && a.vec_ok >= 2 && pos + 8 <= valid)
+                        ldg32_f32(reinterpret_cast<const float*>(src + pos), tmp);
+                    else if (a.vec_ok && pos + 8 <= valid) load_vec<TIn, 8>(src + pos, tmp);
                     else load_vec_guarded<TIn, 8>(src + pos, pos, valid, tmp);
 #pragma unroll
                     for (int r = 0; r < 4; ++r) w[4 * j + r] = tmp[r];
