@@ -460,3 +460,28 @@ def test_dependent_launch_chain_matches_synchronised_chain(port, dtype, b):
 
     for a, b_ in zip(chain(False), chain(True)):
         assert torch.equal(a.contiguous().view(torch.uint8), b_.contiguous().view(torch.uint8))
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("b", [64, 256])
+def test_alignment_variants_are_bit_identical(port, dtype, b):
+    """The same values at 32-byte-aligned (256-bit accesses), 16-byte-aligned and 4/2-byte-
+    aligned addresses give identical messages and decodes (ShardArgs::vec_ok = 2 / 1 / 0)."""
+    n = b * 301
+    cfg = make_config(b)
+    x = torch.from_numpy(port.mixture(n, 31)).to(dtype)
+    esz = x.element_size()
+    ref_msg = codec.compress(x.cuda(), cfg)
+    ref_y = codec.decompress(ref_msg, n, cfg, out_dtype=dtype)
+    for off_bytes in (16, esz, 32):
+        off = off_bytes // esz
+        buf = torch.empty(n + 16, dtype=dtype, device="cuda")
+        buf[off: off + n] = x.cuda()
+        msg = codec.compress(buf[off: off + n], cfg)
+        nb = _abi.msg_layout(cfg, n // b).msg_bytes  # the stride's padding is not written
+        assert torch.equal(msg[:, :nb], ref_msg[:, :nb]), off_bytes
+        ybuf = torch.full((n + 16,), float("nan"), device="cuda").to(dtype)
+        codec.decompress(msg, n, cfg, out=ybuf[off: off + n], out_dtype=dtype)
+        torch.cuda.synchronize()
+        assert torch.equal(ybuf[off: off + n].view(torch.int16 if esz == 2 else torch.int32),
+                           ref_y.view(torch.int16 if esz == 2 else torch.int32)), off_bytes
