@@ -58,6 +58,9 @@ constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capp
 // bf16 keeps the staging (direct loads: 55.7 vs 50.7 us).
 #define TACO_XK_K1_F32_DIRECT 1
 #endif
+#ifndef TACO_XK_K1_L1_DIRECT
+#define TACO_XK_K1_L1_DIRECT 1
+#endif
 #ifndef TACO_XK_SUMSQ_BF16
 #define TACO_XK_SUMSQ_BF16 1  // K1 bf16: sum of squares by fma.rn.f32.bf16 on the inputs (51.35 -> 50.75 us, configs[3])
 #endif
@@ -371,6 +374,16 @@ __device__ __forceinline__ void ldg32_f32(const float* p, float2 (&o)[4]) {
                    "=f"(o[3].y)
                  : "l"(p));
 }
+__device__ __forceinline__ void ldg32_u4x2(const void* p, uint4& a, uint4& b) {
+    asm volatile("ld.global.nc.L1::no_allocate.v8.u32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w), "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w)
+                 : "l"(p));
+}
+__device__ __forceinline__ void stg32_u4x2(void* p, const uint4& a, const uint4& b) {
+    asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(a.x),
+                 "r"(a.y), "r"(a.z), "r"(a.w), "r"(b.x), "r"(b.y), "r"(b.z), "r"(b.w)
+                 : "memory");
+}
 __device__ __forceinline__ void stg32_f32(float* p, const float2* v) {
     asm volatile("st.global.L1::no_allocate.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0].x),
                  "f"(v[0].y), "f"(v[1].x), "f"(v[1].y), "f"(v[2].x), "f"(v[2].y), "f"(v[3].x), "f"(v[3].y)
@@ -407,6 +420,20 @@ __device__ __forceinline__ void store_decoded(T* blk, int q, int valid, int vec_
     using D = DecPlan<L>;
     const int lo = D::lane_off(q);
     if (vec_ok && valid == 64 * L) {
+        if constexpr (L == 1 && sizeof(T) == 2) {  // one lane per block: 64 contiguous outputs
+            if (vec_ok >= 2) {  // (32-byte aligned block starts, see wide_ok)
+#pragma unroll
+                for (int v = 0; v < 8; v += 2) {
+                    static_assert(D::vec_pos(1) == 8, "B = 64 lanes own contiguous 8-element vectors");
+                    const float2* a = &w[4 * v];
+                    const float2* b = &w[4 * v + 4];
+                    stg32_u4x2(blk + D::vec_pos(v),
+                               make_uint4(pack_bf16x2(a[0]), pack_bf16x2(a[1]), pack_bf16x2(a[2]), pack_bf16x2(a[3])),
+                               make_uint4(pack_bf16x2(b[0]), pack_bf16x2(b[1]), pack_bf16x2(b[2]), pack_bf16x2(b[3])));
+                }
+                return;
+            }
+        }
 #pragma unroll
         for (int v = 0; v < 8; ++v) store8<T>(blk + lo + D::vec_pos(v), &w[4 * v], vec_ok >= 2);
     } else {
@@ -444,7 +471,10 @@ struct K1X {
     // fp32 input (TACO_XK_K1_F32_DIRECT): no shared-memory staging -- the lane's chunks are
     // loaded straight into registers (the ragged path's vector loads), which leaves the MIO
     // pipe to the exchanges; 16 warps per SM hide the load latency
-    static constexpr bool DIRECT = sizeof(TIn) == 4 && TACO_XK_K1_F32_DIRECT;
+    // B = 64 bf16 (one lane per block: its 64 inputs are one contiguous 128-byte run) likewise:
+    // the staged form is MIO-bound there (profiles/r3s_block_sweep_configs2.txt)
+    static constexpr bool DIRECT = (sizeof(TIn) == 4 && TACO_XK_K1_F32_DIRECT) ||
+                                   (sizeof(TIn) == 2 && L == 1 && TACO_XK_K1_L1_DIRECT);
     static constexpr int STAGES = DIRECT ? 0 : 2;
     static constexpr int STAGE_U4 = NCH * 32;
 #ifndef TACO_XK_CSTORE
@@ -568,9 +598,23 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 #if TACO_XK_SUMSQ_BF16
             float sq[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #endif
+            uint4 cw[NCH];
+            if constexpr (K::DIRECT) {  // B = 64: the lane's block, straight from global memory
+                const TIn* src = x + (p * a.S + (a.blk0 + kk) * B);
+                if (a.vec_ok >= 2 && (a.P == 1 || (a.S & 15) == 0)) {  // 32-byte aligned block starts
+#pragma unroll
+                    for (int m2 = 0; m2 < NCH / 2; ++m2) ldg32_u4x2(src + 16 * m2, cw[2 * m2], cw[2 * m2 + 1]);
+                } else {
+#pragma unroll
+                    for (int ch = 0; ch < NCH; ++ch) cw[ch] = __ldg(reinterpret_cast<const uint4*>(src + 8 * ch));
+                }
+            } else {
+#pragma unroll
+                for (int ch = 0; ch < NCH; ++ch) cw[ch] = sb[ch * 32];
+            }
 #pragma unroll
             for (int ch = 0; ch < NCH; ++ch) {
-                const uint4 u = sb[ch * 32];
+                const uint4 u = cw[ch];
                 w[4 * ch + 0] = bf16_b0(u.x);
                 w[4 * ch + 1] = bf16_b0(u.y);
                 w[4 * ch + 2] = bf16_b0(u.z);
@@ -782,7 +826,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
         if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
         const uint64_t k = a.blk0 + kk;
         const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
-        store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, a.vec_ok, w);
+        // 256-bit bf16 stores need 32-byte aligned shard starts (S % 16), fp32 ones S % 8 (vec_ok)
+        const int vok = (sizeof(TOut) == 2 && a.P > 1 && (a.S & 15)) ? (a.vec_ok ? 1 : 0) : a.vec_ok;
+        store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, vok, w);
     }
 }
 
