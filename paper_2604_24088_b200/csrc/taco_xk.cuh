@@ -58,8 +58,11 @@ constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capp
 // bf16 keeps the staging (direct loads: 55.7 vs 50.7 us).
 #define TACO_XK_K1_F32_DIRECT 1
 #endif
-#ifndef TACO_XK_K1_L1_DIRECT
-#define TACO_XK_K1_L1_DIRECT 1
+#ifndef TACO_XK_K1_BF16_DIRECT_L
+// bf16 K1 loads straight into registers for these lanes-per-block (bit log2 L): B = 64
+// (LDG.256, 50.3 -> 36.3 us at the configs[2] shape) and B = 128 (42.4 -> 39.4 us); B = 256
+// keeps the cp.async staging (direct: 55.7 vs 50.7 us on configs[3])
+#define TACO_XK_K1_BF16_DIRECT_L 0x3
 #endif
 #ifndef TACO_XK_SUMSQ_BF16
 #define TACO_XK_SUMSQ_BF16 1  // K1 bf16: sum of squares by fma.rn.f32.bf16 on the inputs (51.35 -> 50.75 us, configs[3])
@@ -474,7 +477,7 @@ struct K1X {
     // B = 64 bf16 (one lane per block: its 64 inputs are one contiguous 128-byte run) likewise:
     // the staged form is MIO-bound there (profiles/r3s_block_sweep_configs2.txt)
     static constexpr bool DIRECT = (sizeof(TIn) == 4 && TACO_XK_K1_F32_DIRECT) ||
-                                   (sizeof(TIn) == 2 && L == 1 && TACO_XK_K1_L1_DIRECT);
+                                   (sizeof(TIn) == 2 && ((TACO_XK_K1_BF16_DIRECT_L >> ilog2c(L)) & 1));
     static constexpr int STAGES = DIRECT ? 0 : 2;
     static constexpr int STAGE_U4 = NCH * 32;
 #ifndef TACO_XK_CSTORE
@@ -600,13 +603,13 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
 #endif
             uint4 cw[NCH];
             if constexpr (K::DIRECT) {  // B = 64: the lane's block, straight from global memory
-                const TIn* src = x + (p * a.S + (a.blk0 + kk) * B);
-                if (a.vec_ok >= 2 && (a.P == 1 || (a.S & 15) == 0)) {  // 32-byte aligned block starts
+                const TIn* src = x + (p * a.S + (a.blk0 + kk) * B) + qoff;
+                if (L == 1 && a.vec_ok >= 2 && (a.P == 1 || (a.S & 15) == 0)) {  // 32-byte aligned block starts
 #pragma unroll
                     for (int m2 = 0; m2 < NCH / 2; ++m2) ldg32_u4x2(src + 16 * m2, cw[2 * m2], cw[2 * m2 + 1]);
                 } else {
 #pragma unroll
-                    for (int ch = 0; ch < NCH; ++ch) cw[ch] = __ldg(reinterpret_cast<const uint4*>(src + 8 * ch));
+                    for (int ch = 0; ch < NCH; ++ch) cw[ch] = __ldg(reinterpret_cast<const uint4*>(src + K::chunk_off(ch, 0)));
                 }
             } else {
 #pragma unroll
