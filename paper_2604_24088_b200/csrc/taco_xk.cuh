@@ -58,6 +58,9 @@ constexpr int kMinCtas = TACO_XK_MINCTAS;  // 4: 16 warps per SM (registers capp
 // bf16 keeps the staging (direct loads: 55.7 vs 50.7 us).
 #define TACO_XK_K1_F32_DIRECT 1
 #endif
+#ifndef TACO_XK_K2_DIRECT_L
+#define TACO_XK_K2_DIRECT_L 0x1  // K2 codes straight into registers at B = 64 (33.5 -> 32.1 us at the configs[2] shape); staged elsewhere (B = 256: 36.4 vs 33.1 us direct)
+#endif
 #ifndef TACO_XK_K1_BF16_DIRECT_L
 // bf16 K1 loads straight into registers for these lanes-per-block (bit log2 L): B = 64
 // (LDG.256, 50.3 -> 36.3 us at the configs[2] shape) and B = 128 (42.4 -> 39.4 us); B = 256
@@ -789,7 +792,9 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     const uint32_t ntiles = a.P * tps.d;
     const uint32_t stride = gridDim.x * kWarps;
 
+    constexpr bool DIRECT = (TACO_XK_K2_DIRECT_L >> ilog2c(L)) & 1;  // codes straight into registers
     auto issue = [&](uint32_t tt, int stage) {
+        if (DIRECT) return;
         if (tt < ntiles) {
             const uint32_t p = tps.div(tt);
             const uint64_t kk0 = (uint64_t)(tt - p * tps.d) * G;
@@ -801,37 +806,65 @@ __global__ void __launch_bounds__(kWarps * 32, kMinCtas)
     grid_dep_wait();
     peer_pre(a);  // fused peer mode: every rank's K3 has finished (its messages are in the gather slots)
     uint32_t t = first_tile<TACO_XK_WARP_MAJOR || TACO_XK_K2_WARP_MAJOR>(warp);
+    if constexpr (DIRECT) {
+        for (; t < ntiles; t += stride) {
+            const uint32_t p = tps.div(t);
+            const uint64_t kk = (uint64_t)(t - p * tps.d) * G + g;
+            const bool live = kk < a.nblk;
+            uint4 u[4];
+            float2 sc = make_float2(1.0f, 1.0f);
+            if (live) {  // the lane's 64 codes are one contiguous 64-byte run of the message
+                const uint8_t* m = msgs + p * a.msg_stride;
+                const uint4* src = reinterpret_cast<const uint4*>(m + kk * B + 64 * q);
 #pragma unroll
-    for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
-    int cur = 0;
-    for (; t < ntiles; t += stride) {
-        __syncwarp();  // every lane is done with the stage about to be refilled
-        issue(t + (NS - 1) * stride, cur == 0 ? NS - 1 : cur - 1);
-        const uint32_t p = tps.div(t);
-        const uint64_t kk = (uint64_t)(t - p * tps.d) * G + g;
-        const bool live = kk < a.nblk;
-        cp_wait<NS - 1>();
-        __syncwarp();  // the other lanes' copies of this tile are visible
-        const uint4* sb = stage_base + cur * K::STAGE_U4;
-        cur = cur == NS - 1 ? 0 : cur + 1;
-        uint4 u[4];
-        float2 sc = make_float2(1.0f, 1.0f);
-        if (live) {
-            read_lane_codes<L>(sb, g, q, u);
-            sc = reinterpret_cast<const float2*>(sb + 128)[g];
-        } else {
+                for (int ch = 0; ch < 4; ++ch) u[ch] = __ldg(src + ch);
+                sc = __ldg(reinterpret_cast<const float2*>(m + a.scal_off + kk * 8));
+            } else {
 #pragma unroll
-            for (int ch = 0; ch < 4; ++ch) u[ch] = make_uint4(0, 0, 0, 0);
+                for (int ch = 0; ch < 4; ++ch) u[ch] = make_uint4(0, 0, 0, 0);
+            }
+            float2 w[32];
+            decode_block<L>(u, sc, live, q, c, w);
+            if (!live) continue;
+            if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
+            const uint64_t k = a.blk0 + kk;
+            const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
+            const int vok = (sizeof(TOut) == 2 && a.P > 1 && (a.S & 15)) ? (a.vec_ok ? 1 : 0) : a.vec_ok;
+            store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, vok, w);
         }
-        float2 w[32];
-        decode_block<L>(u, sc, live, q, c, w);
-        if (!live) continue;
-        if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
-        const uint64_t k = a.blk0 + kk;
-        const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
-        // 256-bit bf16 stores need 32-byte aligned shard starts (S % 16), fp32 ones S % 8 (vec_ok)
-        const int vok = (sizeof(TOut) == 2 && a.P > 1 && (a.S & 15)) ? (a.vec_ok ? 1 : 0) : a.vec_ok;
-        store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, vok, w);
+    } else {
+#pragma unroll
+        for (int i = 0; i < NS - 1; ++i) issue(t + i * stride, i);
+        int cur = 0;
+        for (; t < ntiles; t += stride) {
+            __syncwarp();  // every lane is done with the stage about to be refilled
+            issue(t + (NS - 1) * stride, cur == 0 ? NS - 1 : cur - 1);
+            const uint32_t p = tps.div(t);
+            const uint64_t kk = (uint64_t)(t - p * tps.d) * G + g;
+            const bool live = kk < a.nblk;
+            cp_wait<NS - 1>();
+            __syncwarp();  // the other lanes' copies of this tile are visible
+            const uint4* sb = stage_base + cur * K::STAGE_U4;
+            cur = cur == NS - 1 ? 0 : cur + 1;
+            uint4 u[4];
+            float2 sc = make_float2(1.0f, 1.0f);
+            if (live) {
+                read_lane_codes<L>(sb, g, q, u);
+                sc = reinterpret_cast<const float2*>(sb + 128)[g];
+            } else {
+#pragma unroll
+                for (int ch = 0; ch < 4; ++ch) u[ch] = make_uint4(0, 0, 0, 0);
+            }
+            float2 w[32];
+            decode_block<L>(u, sc, live, q, c, w);
+            if (!live) continue;
+            if (q == 0 && !scalars_ok(sc.x, sc.y)) raise_flag(a.flags, 2);
+            const uint64_t k = a.blk0 + kk;
+            const int valid = clamp_valid((int64_t)a.S - (int64_t)(k * B), (int64_t)a.n - (int64_t)(p * a.S + k * B), B);
+            // 256-bit bf16 stores need 32-byte aligned shard starts (S % 16), fp32 ones S % 8 (vec_ok)
+            const int vok = (sizeof(TOut) == 2 && a.P > 1 && (a.S & 15)) ? (a.vec_ok ? 1 : 0) : a.vec_ok;
+            store_decoded<L, TOut>(out + (p * a.S + k * B), q, valid, vok, w);
+        }
     }
 }
 
