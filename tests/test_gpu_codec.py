@@ -485,3 +485,40 @@ def test_alignment_variants_are_bit_identical(port, dtype, b):
         torch.cuda.synchronize()
         assert torch.equal(ybuf[off: off + n].view(torch.int16 if esz == 2 else torch.int32),
                            ref_y.view(torch.int16 if esz == 2 else torch.int32)), off_bytes
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("b", [64, 128])
+def test_direct_load_paths_chunks_and_shards(port, dtype, b):
+    """The register-load K1 / K2 paths (fp32 every B, bf16 B = 64 / 128) over shards whose
+    starts are 32-byte aligned (S % 16 == 0: 256-bit accesses) or only 16-byte aligned
+    (S % 16 == 8), chunks of blocks and a ragged tail: every message equals the compress of
+    the zero-padded slice, chunk messages concatenate to the whole message, and the
+    sharded decode equals the per-shard decodes."""
+    cfg = make_config(b)
+    for shards, S in ((3, b * 40), (2, b * 40 + 8), (4, b * 33 + 16)):
+        n = shards * S - 5  # ragged last shard
+        x = torch.from_numpy(port.mixture(n, 41 + shards)).to(dtype).cuda()
+        Sx = -(-n // shards)
+        m = -(-Sx // b)
+        lay = _abi.msg_layout(cfg, m)
+        sh = codec.compress(x, cfg, shards=shards)
+        for i in range(shards):
+            sl = torch.zeros(Sx, dtype=dtype, device="cuda")
+            seg = x[i * Sx:(i + 1) * Sx]
+            sl[: seg.numel()] = seg
+            one = codec.compress(sl, cfg)
+            assert torch.equal(sh[i, : lay.msg_bytes], one[0, : lay.msg_bytes]), (shards, i)
+        whole = codec.compress(x, cfg)
+        mw = -(-n // b)
+        lw = _abi.msg_layout(cfg, mw)
+        wc, wa, ws = codec.split_message(whole[0], cfg, mw)
+        for b0, b1 in ((0, 7), (7, mw // 2), (mw // 2, mw)):
+            part = codec.compress(x, cfg, blk=(b0, b1))
+            pc, pa, ps = codec.split_message(part[0], cfg, b1 - b0)
+            assert torch.equal(pc, wc[b0 * b: b1 * b]) and torch.equal(pa, wa[b0:b1]) and torch.equal(ps, ws[b0:b1])
+        y = codec.decompress(sh, n, cfg, shards=shards, out_dtype=dtype)
+        want = torch.cat([codec.decompress(sh[i:i + 1], Sx, cfg, out_dtype=dtype) for i in range(shards)])[:n]
+        torch.cuda.synchronize()
+        assert torch.equal(y, want), shards
+        assert lw.msg_bytes > 0
