@@ -609,9 +609,10 @@ def main():
     args.warmup = max(3, args.warmup)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.size_sweep is None:
-        args.size_sweep = [1.0, 16.0, 256.0, 1024.0] if world > 1 else ([1.0, 16.0, 256.0] if args.collective else [])
+        multi = world > 1 or (args.plan and args.gpus > 1)
+        args.size_sweep = [1.0, 16.0, 256.0, 1024.0] if multi else ([1.0, 16.0, 256.0] if args.collective else [])
     rank = int(os.environ.get("RANK", "0"))
-    n_ranks = max(world, args.gpus) if args.impl == "reference" else world
+    n_ranks = max(world, args.gpus) if (args.impl == "reference" or args.plan) else world
     if args.shape:
         args.rows, args.cols = parse_shape(args.shape)
         args.config = None
